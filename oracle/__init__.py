@@ -1,0 +1,257 @@
+"""CPU oracle for the LoBE-GS visibility engine -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+`--impl reference` leg may import, call, link or execute anything under
+oracle/. The product path (paper_2510_01767_b200) never imports it and must
+fail loudly when its CUDA library is missing.
+
+The oracle is a plain scalar C++17 implementation (lobe_oracle.cpp) of
+SURVEY.md §8(c) steps O1-O11, plus a float64 brute-force SPEC-formula
+checker (brute.py). It shares no code with the CUDA path. This module only
+marshals numpy arrays through ctypes and sequences the steps in the order
+the paper defines them.
+
+Parity status per function:
+  validate / frame / prep / cam_setup / visibility (rows, K, z_min, z_max),
+  assign, block_loads, crop: pinned (hand cases, B1 brute force,
+  set enumeration, invariants);
+  depth mean D_c: "parity partially unpinned" -- pinned only by hand case H7
+  and positivity/bounds invariants (no paper values exist, ledger L3/L4).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lobe_oracle.cpp")
+_LIB = os.path.join(_HERE, "liblobe_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+STATUS = {0: "OK", 1: "INVALID_INPUT", 2: "INVALID_CONFIG", 3: "INVALID_CUTS", 4: "INVALID_INDEX",
+          5: "DEGENERATE_SCENE"}
+MODE_RATIO, MODE_HOME, MODE_UNION = 0, 1, 2
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, what=""):
+        super().__init__(f"oracle {what}: {STATUS.get(code, code)}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+def build(force=False):
+    """Compile the oracle with the contract's flags (SURVEY.md §8c 'Build flags')."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread",
+               "-o", _LIB + ".tmp", _SRC]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            _lib = ctypes.CDLL(build())
+    return _lib
+
+
+class _Cam(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_float), ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("R", ctypes.c_float * 9),
+                ("t", ctypes.c_float * 3), ("z_near", ctypes.c_float), ("z_far", ctypes.c_float)]
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def _cams(scene):
+    N = scene.N
+    arr = (_Cam * N)()
+    for c in range(N):
+        k = arr[c]
+        k.fx, k.fy, k.cx, k.cy = (float(scene.fx[c]), float(scene.fy[c]), float(scene.cx[c]), float(scene.cy[c]))
+        k.width, k.height = int(scene.width[c]), int(scene.height[c])
+        k.R[:] = [float(v) for v in scene.R[c].reshape(9)]
+        k.t[:] = [float(v) for v in scene.t[c]]
+        k.z_near, k.z_far = float(scene.z_near[c]), float(scene.z_far[c])
+    return arr
+
+
+def _chk(code, what):
+    if code != 0:
+        raise OracleError(code, what)
+
+
+def nthreads():
+    return int(os.environ.get("LOBE_ORACLE_THREADS", os.cpu_count() or 1))
+
+
+def frame(scene, center=None, radius=None, axis_u=None, axis_v=None):
+    """O2: resolved (c0, rho, a_u, a_v); None -> automatic (ledger L12)."""
+    L = lib()
+    c0 = np.zeros(3, np.float32) if center is None else np.asarray(center, np.float32).copy()
+    rho = ctypes.c_float(0.0 if radius is None else float(radius))
+    au = np.zeros(3, np.float32) if axis_u is None else np.asarray(axis_u, np.float32).copy()
+    av = np.zeros(3, np.float32) if axis_v is None else np.asarray(axis_v, np.float32).copy()
+    flags = (1 if center is None else 0) | (2 if radius is None else 0) | (4 if axis_u is None else 0)
+    if axis_u is None and axis_v is not None:
+        raise ValueError("give both axes or none")
+    cams = _cams(scene)
+    _chk(L.oracle_frame(ctypes.c_int64(scene.N), cams, ctypes.c_uint32(flags), _p(c0), ctypes.byref(rho),
+                        _p(au), _p(av)), "frame")
+    return c0, np.float32(rho.value), au, av
+
+
+def validate(scene):
+    L = lib()
+    bad = ctypes.c_int64(-1)
+    g = [np.ascontiguousarray(a, np.float32) for a in scene.gaussian_arrays()]
+    st = L.oracle_validate_gaussians(ctypes.c_int64(scene.G), *[_p(a) for a in g], ctypes.byref(bad))
+    if st:
+        raise OracleError(st, f"validate gaussians (index {bad.value})")
+    st = L.oracle_validate_cameras(ctypes.c_int64(scene.N), _cams(scene), ctypes.byref(bad))
+    if st:
+        raise OracleError(st, f"validate cameras (index {bad.value})")
+
+
+def prep(scene, fr):
+    """O3 + O4: per-Gaussian k, gate, gu, gv; per-camera setup rows and centre grid coords."""
+    L = lib()
+    c0, rho, au, av = fr
+    G, N = scene.G, scene.N
+    k = np.empty(G, np.float32)
+    gate = np.empty(G, np.uint8)
+    gu = np.empty(G, np.float32)
+    gv = np.empty(G, np.float32)
+    mm = np.empty(4, np.float32)
+    _chk(L.oracle_prep(ctypes.c_int64(G), _p(scene.x), _p(scene.y), _p(scene.z), _p(scene.sx), _p(scene.sy),
+                       _p(scene.sz), _p(scene.opacity), _p(c0), ctypes.c_float(rho), _p(au), _p(av), _p(k),
+                       _p(gate), _p(gu), _p(gv), _p(mm)), "prep")
+    setup = np.empty((N, 16), np.float32)
+    cgu = np.empty(N, np.float32)
+    cgv = np.empty(N, np.float32)
+    _chk(L.oracle_cam_setup(ctypes.c_int64(N), _cams(scene), _p(c0), ctypes.c_float(rho), _p(au), _p(av), _p(mm),
+                            _p(setup), _p(cgu), _p(cgv)), "cam_setup")
+    return dict(k=k, gate=gate, gu=gu, gv=gv, minmax=mm, setup=setup, cam_gu=cgu, cam_gv=cgv)
+
+
+def visibility(scene, pre, cams=None, threads=None):
+    """O6/O7 for the selected cameras (all by default)."""
+    L = lib()
+    G = scene.G
+    sel = None if cams is None else np.ascontiguousarray(cams, np.int64)
+    ns = scene.N if sel is None else int(sel.shape[0])
+    words = (G + 31) // 32
+    rows = np.empty((ns, words), np.uint32)
+    K = np.empty(ns, np.uint32)
+    S = np.empty(ns, np.float64)
+    Om = np.empty(ns, np.float64)
+    zmin = np.empty(ns, np.float32)
+    zmax = np.empty(ns, np.float32)
+    _chk(L.oracle_visibility(ctypes.c_int64(G), _p(scene.x), _p(scene.y), _p(scene.z), _p(pre["k"]),
+                             _p(pre["gate"]), _p(scene.opacity), ctypes.c_int64(ns), _p(sel), _p(pre["setup"]),
+                             _p(rows), _p(K), _p(S), _p(Om), _p(zmin), _p(zmax),
+                             ctypes.c_int(threads or nthreads())), "visibility")
+    with np.errstate(invalid="ignore", divide="ignore"):
+        D = np.where(K > 0, S / np.where(Om > 0, Om, 1.0), 0.0)   # O7
+    return dict(rows=rows, K=K, S=S, Om=Om, D=D, zmin=zmin, zmax=zmax)
+
+
+def default_grid(m, n, v=None, h=None, delta_v=None, delta_h=None, tau=None):
+    """Uniform cuts (v0_i = i/m) and the paper's defaults
+    delta = (0.1/m, 0.1/n) in fp32 (ledger L14), tau = 0.15."""
+    if v is None:
+        v = np.array([np.float32(i / m) for i in range(1, m)], np.float32)
+    if h is None:
+        h = np.array([np.float32(j / n) for j in range(1, n)], np.float32)
+    dv = np.float32(np.float32(0.1) / np.float32(m)) if delta_v is None else np.float32(delta_v)
+    dh = np.float32(np.float32(0.1) / np.float32(n)) if delta_h is None else np.float32(delta_h)
+    return dict(m=m, n=n, v=np.asarray(v, np.float32), h=np.asarray(h, np.float32), dv=dv, dh=dh,
+                tau=0.15 if tau is None else float(tau))
+
+
+def assign(scene, pre, vis, grid, threads=None):
+    L = lib()
+    m, n = grid["m"], grid["n"]
+    B = m * n
+    ns = vis["rows"].shape[0]
+    ncb = np.empty((ns, B), np.uint32)
+    n0 = np.empty((ns, B), np.uint32)
+    member = np.empty(ns, np.uint64)
+    home = np.empty(ns, np.int32)
+    cgu = pre["cam_gu"] if ns == scene.N else pre["cam_gu_sel"]
+    cgv = pre["cam_gv"] if ns == scene.N else pre["cam_gv_sel"]
+    _chk(L.oracle_assign(ctypes.c_int64(scene.G), _p(pre["gu"]), _p(pre["gv"]), ctypes.c_int64(ns),
+                         _p(vis["rows"]), _p(vis["K"]), _p(cgu), _p(cgv), ctypes.c_int(m), ctypes.c_int(n),
+                         _p(grid["v"]), _p(grid["h"]), ctypes.c_float(grid["dv"]), ctypes.c_float(grid["dh"]),
+                         ctypes.c_double(grid["tau"]), _p(ncb), _p(n0), _p(member), _p(home),
+                         ctypes.c_int(threads or nthreads())), "assign")
+    return dict(n=ncb, n0=n0, member=member, home=home)
+
+
+def block_loads(scene, pre, vis, asg, grid, mode=MODE_RATIO, masks=True):
+    L = lib()
+    m, n = grid["m"], grid["n"]
+    B = m * n
+    G = scene.G
+    N = vis["rows"].shape[0]
+    out = dict(n_cams=np.empty(B, np.uint32), g_blk=np.empty(B, np.uint32), g_vis=np.empty(B, np.uint32),
+               incidences=np.empty(B, np.uint64), area=np.empty(B, np.float64), g_avgvis=np.empty(B, np.float64),
+               lohi=np.empty((B, 4), np.float32))
+    M = np.empty((B, (G + 63) // 64), np.uint64) if masks else None
+    obj = ctypes.c_uint32(0)
+    _chk(L.oracle_block_loads(ctypes.c_int64(G), _p(pre["gu"]), _p(pre["gv"]), ctypes.c_int64(N), _p(vis["rows"]),
+                              _p(asg["member"]), _p(asg["home"]), _p(asg["n0"]), ctypes.c_int(m), ctypes.c_int(n),
+                              _p(grid["v"]), _p(grid["h"]), ctypes.c_float(grid["dv"]), ctypes.c_float(grid["dh"]),
+                              ctypes.c_int(mode), _p(out["n_cams"]), _p(out["g_blk"]), _p(out["g_vis"]),
+                              _p(out["incidences"]), _p(out["area"]), _p(out["g_avgvis"]), _p(out["lohi"]), _p(M),
+                              ctypes.byref(obj)), "block_loads")
+    out["objective"] = int(obj.value)
+    out["M"] = M
+    return out
+
+
+def crop(scene, pre, grid, M):
+    L = lib()
+    m, n = grid["m"], grid["n"]
+    B = m * n
+    W = (scene.G + 63) // 64
+    c = np.empty((B, W), np.uint64)
+    e = np.empty((B, W), np.uint64)
+    _chk(L.oracle_crop(ctypes.c_int64(scene.G), _p(pre["gu"]), _p(pre["gv"]), ctypes.c_int(m), ctypes.c_int(n),
+                       _p(grid["v"]), _p(grid["h"]), _p(M), _p(c), _p(e)), "crop")
+    return c, e
+
+
+def run(scene, grid=None, mode=MODE_RATIO, frame_args=None, threads=None, masks=True):
+    """The whole path in the paper's order: validate, frame, per-Gaussian /
+    per-camera setup, visibility, assignment, block loads, crop."""
+    validate(scene)
+    cfg = scene.cfg
+    if grid is None:
+        grid = default_grid(cfg.m, cfg.n)
+    fr = frame(scene, **(frame_args or {}))
+    pre = prep(scene, fr)
+    vis = visibility(scene, pre, threads=threads)
+    asg = assign(scene, pre, vis, grid, threads=threads)
+    bl = block_loads(scene, pre, vis, asg, grid, mode=mode, masks=masks)
+    out = dict(frame=fr, pre=pre, vis=vis, asg=asg, loads=bl, grid=grid)
+    if masks:
+        out["crop"], out["eligible"] = crop(scene, pre, grid, bl["M"])
+    return out
+
+
+def evaluate_cuts(scene, pre, vis, grid, mode=MODE_RATIO):
+    """Objective max_b G_vis for one candidate grid on cached rows (PAPER.md:167,
+    :179 'the back-projection is computed once and reused')."""
+    asg = assign(scene, pre, vis, grid)
+    return block_loads(scene, pre, vis, asg, grid, mode=mode, masks=False)["objective"]
