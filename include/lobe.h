@@ -1,0 +1,250 @@
+/* lobe.h -- C ABI of the B200 visibility engine for LoBE-GS (arXiv 2510.01767).
+ *
+ * The engine computes, for a coarse 3D-Gaussian model and a set of camera views,
+ * the quantities the paper's partitioner needs (§4.1-§4.3):
+ *   - which Gaussians each camera sees (frustum + 3-sigma footprint culling,
+ *     SPEC.md:243, :298-299; ledger L1/L2 in DESIGN.md);
+ *   - a per-camera depth statistic (opacity-weighted mean camera depth, L4);
+ *   - the camera->block assignment C^(b) = {c | V_{c,b} >= tau}
+ *     (Eq. 3), over enlarged regions
+ *     B^(b) = [v_{i-1}-dv, v_i+dv] x [h_{j-1}-dh, h_j+dh];
+ *   - per-block loads A, |C|, G_blk, G_vis, G_avgvis and the
+ *     objective max_b G_vis^(b) (Eq. 2);
+ *   - visibility-cropping and selective-densification masks;
+ *   - the load-balanced cuts by Bayesian optimisation (L = 100).
+ *
+ * Conventions (all calls):
+ *   - Status codes, never exceptions. lobe_last_error() returns a thread-local
+ *     message valid until the next lobe_* call on the calling thread. After a
+ *     failed call outputs are unspecified and the scene handle stays valid.
+ *   - Ownership: the caller owns every pointer it passes. lobe_load_scene copies
+ *     its inputs; the caller may free them on return. Outputs are caller-allocated
+ *     with the sizes stated per call. The scene handle owns its device memory and
+ *     is released by lobe_free_scene.
+ *   - Pointers: output (and, with on_device, input) pointers may be host or
+ *     device pointers (unified addressing decides); device writes are issued on
+ *     lobe_options.stream and every call returns after that stream has drained.
+ *   - Index conventions: Gaussian i is the caller's index; camera c is the
+ *     caller's array index. Block b = p*n + q (0-based), p indexes the v cuts
+ *     (first ground axis), q the h cuts (PAPER.md:165 garbled index read as
+ *     b = (i-1) n + j, ledger L9). B = m*n <= 64. Mask bit (i mod 64) of u64 word
+ *     floor(i/64) is Gaussian i.
+ *   - Multi-GPU: options.rank / options.world select this process's camera shard
+ *     [floor(rN/W), floor((r+1)N/W)) (cameras sharded, Gaussians replicated).
+ *     Per-camera outputs of the calls below cover the LOCAL shard; block-level
+ *     calls that need the other ranks' cameras take the exchanged partials through
+ *     the lobe_*_partial / lobe_*_combine calls; the Python layer
+ *     (paper_2510_01767_b200/engine.py) drives the exchange over torch.distributed
+ *     (NCCL). With world == 1 every call is complete on its own.
+ *   - Concurrency: a handle is not thread-safe; distinct handles are. Every call
+ *     is deterministic (identical inputs give identical bytes, for any world).
+ */
+#ifndef LOBE_H_
+#define LOBE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LOBE_OK = 0,
+  LOBE_E_INVALID_INPUT = 1,     /* non-finite / out-of-range field */
+  LOBE_E_INVALID_CONFIG = 2,    /* zero counts, bad grid, B > 64, bad tau/delta */
+  LOBE_E_INVALID_CUTS = 3,      /* cuts not strictly increasing in (0,1) */
+  LOBE_E_INVALID_INDEX = 4,     /* bad block / camera index */
+  LOBE_E_DEGENERATE_SCENE = 5,  /* all points identical on a ground axis, zero radius */
+  LOBE_E_CUDA = 6,              /* CUDA runtime error or no device */
+  LOBE_E_NCCL = 7,              /* reserved: collective failure reported by the exchange layer */
+  LOBE_E_OOM = 8,               /* device allocation failed */
+  LOBE_E_STATE = 9              /* call out of order (e.g. combine before partial) */
+} lobe_status;
+
+typedef struct lobe_scene lobe_scene; /* opaque */
+
+/* Coarse Gaussians, SoA fp32, caller order (SPEC.md:28-33 Gaussian3D).
+ * s* are per-axis standard deviations (> 0), q* a unit quaternion (|q| = 1
+ * within 1e-6), opacity in [0,1]. |position|, scale <= 1e18 (ledger L22).
+ * on_device != 0: the arrays are device pointers. */
+typedef struct {
+  int64_t n;
+  const float *x, *y, *z, *sx, *sy, *sz, *qw, *qx, *qy, *qz, *opacity;
+  int32_t on_device;
+} lobe_gaussians;
+
+/* Pinhole camera (SPEC.md:44-49 CameraView): world->camera rotation R (row
+ * major) and translation t, p_cam = R p + t, looking along +z_cam; image
+ * width x height pixels; 0 < z_near < z_far. */
+typedef struct {
+  int32_t id;
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9];
+  float t[3];
+  float z_near, z_far;
+} lobe_camera;
+
+/* Normalisation frame for the spherical contraction and ground plane (ledger
+ * L12). auto_flags bit0: centre = component-wise lower median
+ * of camera centres; bit1: radius = ceil(0.9 N)-th smallest camera distance;
+ * bit2: axes = world x, y. Resolved values are written back. */
+#define LOBE_FRAME_AUTO_CENTER 1u
+#define LOBE_FRAME_AUTO_RADIUS 2u
+#define LOBE_FRAME_AUTO_AXES 4u
+#define LOBE_FRAME_AUTO_ALL 7u
+typedef struct {
+  float center[3];
+  float radius;
+  float axis_u[3], axis_v[3];
+  uint32_t auto_flags;
+} lobe_frame;
+
+/* C^(b) selection (ledger L8): RATIO = {c : V_{c,b} >= tau} (PAPER.md:179,
+ * default), HOME = {c : home_c = b}, UNION = both. */
+#define LOBE_ASSIGN_RATIO 0
+#define LOBE_ASSIGN_HOME 1
+#define LOBE_ASSIGN_UNION 2
+
+typedef struct {
+  int32_t device;       /* CUDA device ordinal */
+  int32_t rank, world;  /* camera shard; world >= 1 */
+  void* stream;         /* cudaStream_t; NULL = legacy default stream */
+  int32_t assign_mode;  /* LOBE_ASSIGN_* */
+  int32_t reserved;
+} lobe_options;
+
+/* Grid cuts (GridCuts SPEC.md:51-56). v: m-1 cuts on the first
+ * ground axis, h: n-1 cuts on the second, strictly increasing in (0,1).
+ * delta_v/delta_h < 0 select the paper's (0.1/m, 0.1/n) in fp32 (PAPER.md:167,
+ * ledger L14); tau < 0 selects 0.15. tau is compared in fp64
+ * (ledger L6). */
+typedef struct {
+  int32_t m, n;
+  const float* v;
+  const float* h;
+  float delta_v, delta_h;
+  double tau;
+} lobe_grid;
+
+/* Per-block record (§3.2; BlockLoadStats SPEC.md:232-237).
+ * lo/hi: enlarged region B^(b) (fp32, clamped to [0,1]); area: delta = 0 cell
+ * area in fp64; incidences: sum_c n0_{c,b}. */
+typedef struct {
+  int32_t block_id, row, col;
+  float lo[2], hi[2];
+  double area;
+  uint32_t n_cams, g_blk, g_vis;
+  double g_avgvis;
+  uint64_t incidences;
+} lobe_block_load;
+
+/* BO options. L <= 0 -> 100; n_sobol < 0 -> 8;
+ * delta_scale <= 0 -> 0.1 (delta = delta_scale/m, delta_scale/n); tau < 0 -> 0.15. */
+typedef struct {
+  int32_t L;
+  uint64_t seed;
+  float delta_scale;
+  double tau;
+  int32_t n_sobol;
+} lobe_balance_opts;
+
+/* Stage timings of the last call (CUDA events on options.stream), cumulative
+ * logical Gaussian-camera tests executed by the visibility kernel (I16), and
+ * algorithmic bytes of the last visibility pass. */
+typedef struct {
+  double t_prep_ms, t_vis_ms, t_hist_ms, t_loads_ms, t_comm_ms, t_crop_ms;
+  uint64_t tests_executed, bytes_read, bytes_written;
+  uint64_t vis_launches, evaluations;
+  int64_t n_gaussians, n_cameras, n_local_cameras, cam_begin;
+  uint64_t tile_pairs; /* (tile, camera) pairs with any visible Gaussian */
+} lobe_stats;
+
+/* ---- scene --------------------------------------------------------------- */
+
+/* Validate, resolve the frame, precompute per-Gaussian data (contraction,
+ * grid coords, footprint radius, opacity gate, spatial sort) and per-camera
+ * projection rows, then run the visibility pass once for the local cameras
+ * (rows, K_c, depth sums). Everything after this reuses the cached rows
+ * ("the back-projection is computed once and reused").
+ * inout_frame may be NULL (= LOBE_FRAME_AUTO_ALL). */
+lobe_status lobe_load_scene(const lobe_gaussians* gaussians, const lobe_camera* cameras, int64_t n_cams,
+                            lobe_frame* inout_frame, const lobe_options* options, lobe_scene** out);
+void lobe_free_scene(lobe_scene* scene);
+const char* lobe_last_error(void);
+
+/* ---- per-camera outputs (local shard: n_local entries, see lobe_get_stats) -- */
+
+/* K_c, depth mean D_c = sum(o w)/sum(o) over V_c (0 if K_c = 0, ledger L4/L7),
+ * z_min/z_max over V_c (+inf/-inf if K_c = 0); n_cb/n0_cb: n_local x B counts of
+ * V_c inside the enlarged regions / delta = 0 cells;
+ * member: bit b set iff K_c > 0 and n_cb >= tau K_c;
+ * home: lowest b maximising n0_cb, camera-centre cell if K_c = 0 (ledger L7/L8).
+ * Any output pointer may be NULL. */
+lobe_status lobe_assign_cameras(lobe_scene* scene, const lobe_grid* grid, uint32_t* K, double* depth_mean,
+                                float* z_min, float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member,
+                                int32_t* home);
+
+/* ---- block loads (world == 1: complete) ---------------------------------- */
+
+/* out: B records; objective: max_b g_vis. */
+lobe_status lobe_block_loads(lobe_scene* scene, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective);
+
+/* crop, eligible: B x ceil(G/64) u64, caller order. crop_b = union of the rows
+ * of C^(b) (visibility cropping); eligible_b = crop_b and
+ * "centre in the delta = 0 cell of b" (selective densification).
+ * Either may be NULL. */
+lobe_status lobe_crop_masks(lobe_scene* scene, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible);
+
+/* Load-balanced cuts: uniform cuts first, then n_sobol
+ * scrambled Sobol points, then GP (Matern-5/2 ARD) + expected improvement, L
+ * evaluations in total, each cut bounded to move at most halfway to its
+ * neighbours. v_out: m-1, h_out: n-1 floats; history: L objective values
+ * (may be NULL); cut_history: L x (m+n-2) floats (may be NULL); best: B records
+ * at the returned cuts (may be NULL). world == 1 only; multi-rank runs use
+ * lobe_bo_run with the exchange layer's objective. */
+lobe_status lobe_balance_partition(lobe_scene* scene, int32_t m, int32_t n, const lobe_balance_opts* opts,
+                                   float* v_out, float* h_out, uint32_t* history, float* cut_history,
+                                   lobe_block_load* best);
+
+/* Host-only BO driver with a caller objective (the same driver the call above
+ * uses). objective(ctx, v, h, out_value) returns 0 on success. Needs no GPU. */
+typedef int (*lobe_objective_fn)(void* ctx, const float* v, const float* h, uint32_t* out_value);
+lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lobe_objective_fn objective, void* ctx,
+                        float* v_out, float* h_out, uint32_t* history, float* cut_history);
+
+/* ---- multi-rank exchange points (used by engine.py when world > 1) ------- */
+
+/* Rank-local part of lobe_block_loads: d_masks (DEVICE, B x lobe_mask_words
+ * u32, internal Gaussian order) receives OR over the LOCAL cameras of C^(b);
+ * n_cams / incid (B entries, host or device) the local counts. */
+size_t lobe_mask_words(const lobe_scene* scene);
+lobe_status lobe_block_partial(lobe_scene* scene, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
+                               uint64_t* incid);
+/* OR the W gathered partial mask sets (DEVICE, W x B x lobe_mask_words u32,
+ * rank-major) into d_out (DEVICE, B x words) and popcount each block into g_vis
+ * (B entries). d_out may alias d_gathered. */
+lobe_status lobe_masks_combine(lobe_scene* scene, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
+                               uint32_t* g_vis);
+/* Assemble B records from global counts (areas, regions, G_blk from the scene). */
+lobe_status lobe_block_records(lobe_scene* scene, const lobe_grid* grid, const uint32_t* n_cams,
+                               const uint64_t* incid, const uint32_t* g_vis, lobe_block_load* out,
+                               uint32_t* objective);
+/* Crop / eligible masks (caller order) from combined masks d_masks (DEVICE). */
+lobe_status lobe_crop_from_masks(lobe_scene* scene, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
+                                 uint64_t* eligible);
+
+/* ---- introspection / tests ----------------------------------------------- */
+
+/* Visibility rows of local cameras [c0, c0 + count) in caller Gaussian order:
+ * count x ceil(G/32) u32, bit (i mod 32) of word i/32 (for parity tests). */
+lobe_status lobe_export_rows(lobe_scene* scene, int64_t c0, int64_t count, uint32_t* rows);
+lobe_status lobe_get_stats(const lobe_scene* scene, lobe_stats* out);
+/* Library build info string (arch, flags). */
+const char* lobe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOBE_H_ */

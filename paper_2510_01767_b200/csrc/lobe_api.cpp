@@ -1,0 +1,942 @@
+// lobe_api.cpp -- host runtime behind include/lobe.h.
+//
+// Owns the scene's device memory (stream-ordered pool allocations), validates
+// inputs, resolves the frame and the per-camera projection rows (host fp64,
+// rounded once to fp32 -- ledger L13), sequences the kernels of
+// lobe_kernels.cu and caches the last evaluated grid so that assign / loads /
+// crop calls on the same cuts reuse one evaluation. Compiled with
+// -ffp-contract=off: the few fp32 host operations (camera-centre grid
+// coordinates, region bounds) are single IEEE operations in the order written.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include <functional>
+
+#include <cuda_runtime.h>
+
+#include "../../include/lobe.h"
+#include "lobe_internal.h"
+
+using namespace lobe;
+
+namespace lobe {
+// lobe_bo.cpp
+int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
+           const std::function<int(const float*, const float*, uint32_t*)>& objective, float* v_out, float* h_out,
+           uint32_t* history, float* cut_history, std::string* err);
+}  // namespace lobe
+
+namespace {
+
+thread_local std::string g_err;
+
+lobe_status fail(lobe_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      return fail(e_ == cudaErrorMemoryAllocation ? LOBE_E_OOM : LOBE_E_CUDA,                      \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                             \
+    }                                                                                              \
+  } while (0)
+
+#define TRY(expr)                       \
+  do {                                  \
+    lobe_status s_ = (expr);            \
+    if (s_ != LOBE_OK) return s_;       \
+  } while (0)
+
+const double kMag = 1e18;  // ledger L22
+
+inline bool in_interval(float x, float lo, float hi) {
+  return x >= lo && (x < hi || (hi == 1.0f && x <= 1.0f));
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct lobe_scene {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1, assign_mode = 0;
+  int num_sms = 148;
+  int64_t G = 0, G_pad = 0, N_all = 0, N_loc = 0, cam_begin = 0;
+  int64_t words = 0, n_tiles = 0, n_chunks = 0;
+  lobe_frame frame{};
+  float mm[4] = {0, 0, 0, 0};
+  std::vector<float> cam_gu, cam_gv;
+  // device, internal order
+  float *xy = nullptr, *zk = nullptr, *o2 = nullptr, *gu = nullptr, *gv = nullptr;
+  int32_t* iperm = nullptr;
+  CamSetup* cams = nullptr;
+  float *d_cam_gu = nullptr, *d_cam_gv = nullptr;
+  uint32_t* rows = nullptr;
+  uint8_t* flags = nullptr;
+  VisPartial* part = nullptr;
+  uint32_t* K = nullptr;
+  double* D = nullptr;
+  float *zmin = nullptr, *zmax = nullptr;
+  uint32_t *tile_off = nullptr, *pair_cam = nullptr, *pair_tile = nullptr;
+  int64_t n_pairs = 0;
+  // evaluation scratch
+  uint16_t *zp = nullptr, *word_zone = nullptr, *tile_zone = nullptr;
+  uint32_t* zp_count = nullptr;
+  ZoneTables* dz = nullptr;
+  uint8_t* d_zp_cell = nullptr;
+  uint32_t* hist = nullptr;
+  size_t hist_cap = 0;
+  uint32_t *ncb = nullptr, *n0cb = nullptr;
+  uint64_t *member = nullptr, *sel = nullptr;
+  int32_t* home = nullptr;
+  uint32_t* counts = nullptr;  // [0:64) ncams, [64:128) gvis, [128:192) gblk
+  unsigned long long* incid = nullptr;  // [64]
+  uint32_t* masks = nullptr;
+  int masks_B = 0;
+  // cache of the last evaluated grid
+  bool ev_valid = false;
+  int ev_m = 0, ev_n = 0, ev_mode = 0;
+  std::vector<float> ev_v, ev_h;
+  float ev_dv = 0, ev_dh = 0;
+  double ev_tau = 0;
+  ZoneTables hz{};
+  std::vector<uint8_t> zp_cell;
+  uint32_t h_ncams[kMaxBlocks], h_gvis[kMaxBlocks], h_gblk[kMaxBlocks];
+  unsigned long long h_incid[kMaxBlocks];
+  // stats
+  lobe_stats st{};
+  cudaEvent_t ev[8] = {};
+
+  template <class T>
+  cudaError_t alloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), stream);
+  }
+  template <class T>
+  void release(T*& p) {
+    if (p) cudaFreeAsync(p, stream);
+    p = nullptr;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- validation
+lobe_status validate_cameras(const lobe_camera* cams, int64_t N) {
+  if (N <= 0) return fail(LOBE_E_INVALID_CONFIG, "n_cams must be > 0 (SPEC.md:110)");
+  for (int64_t c = 0; c < N; ++c) {
+    const lobe_camera& k = cams[c];
+    bool ok = std::isfinite(k.fx) && std::isfinite(k.fy) && std::isfinite(k.cx) && std::isfinite(k.cy) &&
+              k.fx > 0.0f && k.fy > 0.0f && k.width > 0 && k.height > 0 && std::isfinite(k.z_near) &&
+              std::isfinite(k.z_far) && k.z_near > 0.0f && k.z_near < k.z_far &&
+              std::fabs((double)k.cx) <= kMag && std::fabs((double)k.cy) <= kMag;
+    for (int j = 0; j < 3; ++j) ok = ok && std::isfinite(k.t[j]) && std::fabs((double)k.t[j]) <= kMag;
+    for (int j = 0; j < 9; ++j) ok = ok && std::isfinite(k.R[j]);
+    for (int a = 0; ok && a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double d = (double)k.R[3 * a] * k.R[3 * b] + (double)k.R[3 * a + 1] * k.R[3 * b + 1] +
+                   (double)k.R[3 * a + 2] * k.R[3 * b + 2];
+        if (std::fabs(d - (a == b ? 1.0 : 0.0)) > 1e-5) ok = false;
+      }
+    if (!ok)
+      return fail(LOBE_E_INVALID_INPUT,
+                  "camera " + std::to_string(c) + " invalid (fx,fy>0, 0<z_near<z_far, R orthonormal; SPEC.md:46-48)");
+  }
+  return LOBE_OK;
+}
+
+// camera centre o = -R^T t in fp64
+void cam_centre(const lobe_camera& k, double o[3]) {
+  for (int j = 0; j < 3; ++j)
+    o[j] = -((double)k.R[j] * k.t[0] + (double)k.R[3 + j] * k.t[1] + (double)k.R[6 + j] * k.t[2]);
+}
+
+// Ledger L12: lower median centre, ceil(0.9 N)-th smallest distance, world x/y axes.
+lobe_status resolve_frame(const lobe_camera* cams, int64_t N, lobe_frame* f) {
+  std::vector<double> c[3];
+  for (int a = 0; a < 3; ++a) c[a].resize(N);
+  for (int64_t i = 0; i < N; ++i) {
+    double o[3];
+    cam_centre(cams[i], o);
+    for (int a = 0; a < 3; ++a) c[a][i] = o[a];
+  }
+  if (f->auto_flags & LOBE_FRAME_AUTO_CENTER) {
+    for (int a = 0; a < 3; ++a) {
+      std::vector<double> s = c[a];
+      std::nth_element(s.begin(), s.begin() + (N - 1) / 2, s.end());
+      f->center[a] = (float)s[(N - 1) / 2];
+    }
+  }
+  if (f->auto_flags & LOBE_FRAME_AUTO_RADIUS) {
+    std::vector<double> d(N);
+    for (int64_t i = 0; i < N; ++i) {
+      double dx = c[0][i] - (double)f->center[0], dy = c[1][i] - (double)f->center[1],
+             dz = c[2][i] - (double)f->center[2];
+      d[i] = std::sqrt(dx * dx + dy * dy + dz * dz);
+    }
+    const int64_t kth = (9 * N + 9) / 10;  // ceil(0.9 N)
+    std::nth_element(d.begin(), d.begin() + (kth - 1), d.end());
+    f->radius = (float)d[kth - 1];
+  }
+  if (f->auto_flags & LOBE_FRAME_AUTO_AXES) {
+    const float u[3] = {1, 0, 0}, v[3] = {0, 1, 0};
+    std::memcpy(f->axis_u, u, sizeof(u));
+    std::memcpy(f->axis_v, v, sizeof(v));
+  }
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(f->center[a]) || !std::isfinite(f->axis_u[a]) || !std::isfinite(f->axis_v[a]))
+      return fail(LOBE_E_INVALID_INPUT, "frame centre/axes not finite");
+  if (!(f->radius > 0.0f) || !std::isfinite(f->radius))
+    return fail(LOBE_E_DEGENERATE_SCENE, "frame radius is zero (all cameras at one point)");
+  return LOBE_OK;
+}
+
+// scaled rows in fp64, rounded once (L13).
+CamSetup camera_setup(const lobe_camera& k) {
+  const double f = (double)std::max(k.fx, k.fy);
+  CamSetup s;
+  for (int j = 0; j < 3; ++j) {
+    s.Au[j] = (float)(((double)k.fx * k.R[j] + (double)k.cx * k.R[6 + j]) / f);
+    s.Av[j] = (float)(((double)k.fy * k.R[3 + j] + (double)k.cy * k.R[6 + j]) / f);
+    s.Aw[j] = k.R[6 + j];
+  }
+  s.Au[3] = (float)(((double)k.fx * k.t[0] + (double)k.cx * k.t[2]) / f);
+  s.Av[3] = (float)(((double)k.fy * k.t[1] + (double)k.cy * k.t[2]) / f);
+  s.Aw[3] = k.t[2];
+  s.Wf = (float)((double)k.width / f);
+  s.Hf = (float)((double)k.height / f);
+  s.zn = k.z_near;
+  s.zf = k.z_far;
+  return s;
+}
+
+// O3's fp32 map for one point (contraction + ground projection), host side.
+void ground_uv_host(float px, float py, float pz, const lobe_frame& F, float* gu, float* gv) {
+  float hx = (px - F.center[0]) / F.radius;
+  float hy = (py - F.center[1]) / F.radius;
+  float hz = (pz - F.center[2]) / F.radius;
+  float r = std::sqrt(std::fmaf(hx, hx, std::fmaf(hy, hy, hz * hz)));
+  if (!(r <= 1.0f)) {
+    float s = (2.0f - 1.0f / r) / r;
+    hx = hx * s;
+    hy = hy * s;
+    hz = hz * s;
+  }
+  *gu = std::fmaf(hx, F.axis_u[0], std::fmaf(hy, F.axis_u[1], hz * F.axis_u[2]));
+  *gv = std::fmaf(hx, F.axis_v[0], std::fmaf(hy, F.axis_v[1], hz * F.axis_v[2]));
+}
+
+// ------------------------------------------------------------- grid / zones
+struct GridV {
+  int m, n, B;
+  std::vector<float> v, h;
+  float dv, dh;
+  double tau;
+};
+
+lobe_status check_grid(const lobe_grid* g, GridV* out) {
+  if (!g) return fail(LOBE_E_INVALID_CONFIG, "grid is NULL");
+  if (g->m < 1 || g->n < 1 || (int64_t)g->m * g->n > kMaxBlocks)
+    return fail(LOBE_E_INVALID_CONFIG, "grid m, n must be >= 1 with m*n <= 64");
+  out->m = g->m;
+  out->n = g->n;
+  out->B = g->m * g->n;
+  out->v.assign(g->v ? g->v : nullptr, g->v ? g->v + (g->m - 1) : nullptr);
+  out->h.assign(g->h ? g->h : nullptr, g->h ? g->h + (g->n - 1) : nullptr);
+  if ((g->m > 1 && !g->v) || (g->n > 1 && !g->h)) return fail(LOBE_E_INVALID_CUTS, "missing cut array");
+  for (int i = 0; i + 1 < g->m; ++i)
+    if (!(out->v[i] > 0.0f && out->v[i] < 1.0f) || (i > 0 && !(out->v[i] > out->v[i - 1])))
+      return fail(LOBE_E_INVALID_CUTS, "v cuts must be strictly increasing in (0,1) (SPEC.md:52-55)");
+  for (int j = 0; j + 1 < g->n; ++j)
+    if (!(out->h[j] > 0.0f && out->h[j] < 1.0f) || (j > 0 && !(out->h[j] > out->h[j - 1])))
+      return fail(LOBE_E_INVALID_CUTS, "h cuts must be strictly increasing in (0,1) (SPEC.md:52-55)");
+  out->dv = g->delta_v < 0.0f ? 0.1f / (float)g->m : g->delta_v;  // PAPER.md:167, ledger L14
+  out->dh = g->delta_h < 0.0f ? 0.1f / (float)g->n : g->delta_h;
+  out->tau = g->tau < 0.0 ? 0.15 : g->tau;
+  if (!std::isfinite(out->dv) || !std::isfinite(out->dh)) return fail(LOBE_E_INVALID_CONFIG, "delta not finite");
+  if (!(out->tau >= 0.0 && out->tau <= 1.0)) return fail(LOBE_E_INVALID_CONFIG, "tau must be in [0,1]");
+  return LOBE_OK;
+}
+
+// Zones of one axis: breakpoints of all cell and enlarged-region
+// bounds; every point of a zone has the same cell and enlarged memberships.
+void build_axis(int count, const std::vector<float>& cuts, float delta, AxisZones* A) {
+  std::vector<float> lo(count), hi(count), elo(count), ehi(count);
+  std::vector<float> P = {0.0f};
+  for (int p = 0; p < count; ++p) {
+    lo[p] = (p == 0) ? 0.0f : cuts[p - 1];
+    hi[p] = (p == count - 1) ? 1.0f : cuts[p];
+    elo[p] = std::fmax(0.0f, lo[p] - delta);
+    ehi[p] = std::fmin(1.0f, hi[p] + delta);
+    for (float b : {lo[p], hi[p], elo[p], ehi[p]})
+      if (b < 1.0f) P.push_back(b);
+  }
+  std::sort(P.begin(), P.end());
+  P.erase(std::unique(P.begin(), P.end()), P.end());
+  const int K = (int)P.size();
+  A->nz = K + 1;
+  A->count = count;
+  for (int z = 0; z < A->nz; ++z) {
+    const float rep = (z < K) ? P[z] : 1.0f;
+    if (z < K) A->P[z] = P[z];
+    A->cell[z] = 0;
+    A->encl[z] = 0;
+    for (int p = 0; p < count; ++p) {
+      if (in_interval(rep, lo[p], hi[p])) A->cell[z] = (uint8_t)p;
+      if (in_interval(rep, elo[p], ehi[p])) A->encl[z] |= 1ull << p;
+    }
+  }
+}
+
+int cell_host(const AxisZones& A, float x) {
+  if (x == 1.0f) return A.cell[A.nz - 1];
+  int z = 0;
+  for (int k = 1; k < A.nz - 1; ++k) z += (A.P[k] <= x) ? 1 : 0;
+  return A.cell[z];
+}
+
+lobe_status ensure_hist_cap(lobe_scene* s, size_t need) {
+  if (s->hist_cap >= need) return LOBE_OK;
+  s->release(s->hist);
+  CK(s->alloc(&s->hist, need));
+  s->hist_cap = need;
+  return LOBE_OK;
+}
+
+lobe_status ensure_masks(lobe_scene* s, int B) {
+  if (s->masks && s->masks_B >= B) return LOBE_OK;
+  s->release(s->masks);
+  CK(s->alloc(&s->masks, (size_t)B * s->words));
+  s->masks_B = B;
+  return LOBE_OK;
+}
+
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0.f;
+  return ms;
+}
+
+// a5 + a6 + a7 (+ a8 into `masks_out`): one evaluation of a grid on cached rows.
+lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
+  cudaStream_t st = s->stream;
+  // ---- a5 zone tables (host) + per-Gaussian zones (device)
+  ZoneTables Z{};
+  build_axis(g.m, g.v, g.dv, &Z.U);
+  build_axis(g.n, g.h, g.dh, &Z.V);
+  Z.m = g.m;
+  Z.n = g.n;
+  Z.B = g.B;
+  const int nzv = Z.V.nz, nzp = Z.U.nz * Z.V.nz;
+  s->hz = Z;
+  s->zp_cell.assign(nzp, 0);
+  for (int zp = 0; zp < nzp; ++zp) s->zp_cell[zp] = (uint8_t)(Z.U.cell[zp / nzv] * g.n + Z.V.cell[zp % nzv]);
+  CK(cudaMemcpyAsync(s->dz, &Z, sizeof(Z), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->d_zp_cell, s->zp_cell.data(), nzp, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(s->zp_count, 0, sizeof(uint32_t) * kMaxZones * kMaxZones, st));
+  CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks, st));
+  CK(cudaMemsetAsync(s->incid, 0, sizeof(unsigned long long) * kMaxBlocks, st));
+  CK(cudaEventRecord(s->ev[2], st));
+  CK(launch_zones(s->dz, nzv, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
+  CK(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
+  // ---- a6 histograms
+  TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
+  if (s->N_loc > 0) {
+    CK(cudaMemsetAsync(s->hist, 0, sizeof(uint32_t) * (size_t)s->N_loc * nzp, st));
+    CK(launch_hist(s->n_pairs, s->pair_cam, s->pair_tile, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
+                   s->hist, st));
+  }
+  CK(cudaEventRecord(s->ev[3], st));
+  // ---- a7 assignment
+  if (s->N_loc > 0) {
+    AssignArgs a{};
+    a.dz = s->dz;
+    a.hist = s->hist;
+    a.nzp = nzp;
+    a.K = s->K;
+    a.cam_gu = s->d_cam_gu;
+    a.cam_gv = s->d_cam_gv;
+    a.n_cams = s->N_loc;
+    a.tau = g.tau;
+    a.mode = s->assign_mode;
+    a.ncb = s->ncb;
+    a.n0cb = s->n0cb;
+    a.member = s->member;
+    a.home = s->home;
+    a.sel = s->sel;
+    a.ncams = s->counts;
+    a.incid = s->incid;
+    CK(launch_assign(a, st));
+  }
+  // ---- a8 block masks
+  if (masks_out) {
+    CK(launch_block_masks(s->n_tiles, s->tile_off, s->pair_cam, s->sel, s->rows, s->words, g.B, masks_out,
+                          s->counts + kMaxBlocks, st));
+  }
+  CK(cudaEventRecord(s->ev[4], st));
+  CK(cudaMemcpyAsync(s->h_ncams, s->counts, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s->h_gvis, s->counts + kMaxBlocks, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s->h_gblk, s->counts + 2 * kMaxBlocks, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost,
+                     st));
+  CK(cudaMemcpyAsync(s->h_incid, s->incid, sizeof(unsigned long long) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s->st.t_hist_ms = ms_between(s->ev[2], s->ev[3]);
+  s->st.t_loads_ms = ms_between(s->ev[3], s->ev[4]);
+  s->st.evaluations += 1;
+  return LOBE_OK;
+}
+
+bool same_grid(const lobe_scene* s, const GridV& g) {
+  return s->ev_valid && s->ev_m == g.m && s->ev_n == g.n && s->ev_v == g.v && s->ev_h == g.h &&
+         s->ev_dv == g.dv && s->ev_dh == g.dh && s->ev_tau == g.tau && s->ev_mode == s->assign_mode;
+}
+
+// world == 1 path: evaluation into the scene's own mask buffer, cached.
+lobe_status ensure_eval(lobe_scene* s, const GridV& g) {
+  if (same_grid(s, g)) return LOBE_OK;
+  s->ev_valid = false;
+  TRY(ensure_masks(s, g.B));
+  TRY(evaluate(s, g, s->masks));
+  s->ev_valid = true;
+  s->ev_m = g.m;
+  s->ev_n = g.n;
+  s->ev_v = g.v;
+  s->ev_h = g.h;
+  s->ev_dv = g.dv;
+  s->ev_dh = g.dh;
+  s->ev_tau = g.tau;
+  s->ev_mode = s->assign_mode;
+  return LOBE_OK;
+}
+
+void fill_records(const lobe_scene* s, const GridV& g, const uint32_t* ncams, const uint64_t* incid,
+                  const uint32_t* gvis, lobe_block_load* out, uint32_t* objective) {
+  std::vector<float> ulo(g.m), uhi(g.m), uelo(g.m), uehi(g.m), vlo(g.n), vhi(g.n), velo(g.n), vehi(g.n);
+  for (int p = 0; p < g.m; ++p) {
+    ulo[p] = (p == 0) ? 0.0f : g.v[p - 1];
+    uhi[p] = (p == g.m - 1) ? 1.0f : g.v[p];
+    uelo[p] = std::fmax(0.0f, ulo[p] - g.dv);
+    uehi[p] = std::fmin(1.0f, uhi[p] + g.dv);
+  }
+  for (int q = 0; q < g.n; ++q) {
+    vlo[q] = (q == 0) ? 0.0f : g.h[q - 1];
+    vhi[q] = (q == g.n - 1) ? 1.0f : g.h[q];
+    velo[q] = std::fmax(0.0f, vlo[q] - g.dh);
+    vehi[q] = std::fmin(1.0f, vhi[q] + g.dh);
+  }
+  uint32_t best = 0;
+  for (int b = 0; b < g.B; ++b) {
+    const int p = b / g.n, q = b % g.n;
+    lobe_block_load r{};
+    r.block_id = b;
+    r.row = p;
+    r.col = q;
+    r.lo[0] = uelo[p];
+    r.lo[1] = velo[q];
+    r.hi[0] = uehi[p];
+    r.hi[1] = vehi[q];
+    r.area = ((double)uhi[p] - (double)ulo[p]) * ((double)vhi[q] - (double)vlo[q]);
+    r.n_cams = ncams[b];
+    r.g_blk = s->h_gblk[b];
+    r.g_vis = gvis[b];
+    r.g_avgvis = r.n_cams ? (double)r.g_vis / (double)r.n_cams : 0.0;
+    r.incidences = incid[b];
+    best = std::max(best, r.g_vis);
+    if (out) out[b] = r;
+  }
+  if (objective) *objective = best;
+}
+
+lobe_status copy_out(lobe_scene* s, void* dst, const void* src, size_t bytes) {
+  if (!dst || bytes == 0) return LOBE_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->stream));
+  return LOBE_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* lobe_last_error(void) { return g_err.c_str(); }
+
+const char* lobe_version(void) {
+  return "lobe 0.1 sm_100a (-fmad=false, IEEE div/sqrt, FFMA2 visibility, tile lists)";
+}
+
+size_t lobe_mask_words(const lobe_scene* s) { return s ? (size_t)s->words : 0; }
+
+void lobe_free_scene(lobe_scene* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
+  s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
+  s->release(s->rows); s->release(s->flags); s->release(s->part); s->release(s->K); s->release(s->D);
+  s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
+  s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
+  s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
+  s->release(s->ncb); s->release(s->n0cb); s->release(s->member); s->release(s->sel); s->release(s->home);
+  s->release(s->counts); s->release(s->incid); s->release(s->masks);
+  cudaStreamSynchronize(s->stream);
+  for (auto& e : s->ev)
+    if (e) cudaEventDestroy(e);
+  delete s;
+}
+
+lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, int64_t n_cams, lobe_frame* inout_frame,
+                            const lobe_options* opt, lobe_scene** out) {
+  g_err.clear();
+  if (!out) return fail(LOBE_E_INVALID_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (!g || !cams) return fail(LOBE_E_INVALID_CONFIG, "gaussians/cameras NULL");
+  if (g->n <= 0) return fail(LOBE_E_INVALID_CONFIG, "gaussian count must be > 0 (SPEC.md:110)");
+  if (g->n > (int64_t)INT32_MAX - 2 * kChunk) return fail(LOBE_E_INVALID_CONFIG, "too many Gaussians");
+  lobe_options o{};
+  o.world = 1;
+  if (opt) o = *opt;
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(LOBE_E_INVALID_CONFIG, "bad rank/world");
+  if (o.assign_mode < 0 || o.assign_mode > 2) return fail(LOBE_E_INVALID_CONFIG, "bad assign_mode");
+  TRY(validate_cameras(cams, n_cams));
+  lobe_frame F{};
+  if (inout_frame) F = *inout_frame;
+  else F.auto_flags = LOBE_FRAME_AUTO_ALL;
+  TRY(resolve_frame(cams, n_cams, &F));
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LOBE_E_CUDA, "no CUDA device");
+  CK(cudaSetDevice(o.device));
+  {  // keep freed pool memory for the next scene (stream-ordered allocator)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  lobe_scene* s = new lobe_scene();
+  s->device = o.device;
+  s->stream = static_cast<cudaStream_t>(o.stream);
+  s->rank = o.rank;
+  s->world = o.world;
+  s->assign_mode = o.assign_mode;
+  s->frame = F;
+  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, o.device);
+  for (auto& e : s->ev) cudaEventCreate(&e);
+  lobe_status rs = [&]() -> lobe_status {
+    cudaStream_t st = s->stream;
+    const int64_t G = g->n;
+    s->G = G;
+    s->G_pad = (G + kChunk - 1) / kChunk * kChunk;
+    s->words = s->G_pad / 32;
+    s->n_tiles = s->G_pad / kTile;
+    s->n_chunks = s->G_pad / kChunk;
+    s->N_all = n_cams;
+    s->cam_begin = (int64_t)o.rank * n_cams / o.world;
+    const int64_t cam_end = (int64_t)(o.rank + 1) * n_cams / o.world;
+    s->N_loc = cam_end - s->cam_begin;
+
+    CK(cudaEventRecord(s->ev[0], st));
+    // ---- inputs on device
+    const float* src[11] = {g->x, g->y, g->z, g->sx, g->sy, g->sz, g->qw, g->qx, g->qy, g->qz, g->opacity};
+    for (int k = 0; k < 11; ++k)
+      if (!src[k]) return fail(LOBE_E_INVALID_CONFIG, "gaussian array NULL");
+    float* dev_in = nullptr;
+    const float* din[11];
+    if (!g->on_device) {
+      CK(s->alloc(&dev_in, (size_t)11 * G));
+      for (int k = 0; k < 11; ++k) {
+        CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
+        din[k] = dev_in + (size_t)k * G;
+      }
+    } else {
+      for (int k = 0; k < 11; ++k) din[k] = src[k];
+    }
+    // ---- a1 precompute
+    float *ru, *rv, *kk, *gu_c, *gv_c;
+    uint32_t *keys, *keys_s, *scratch;
+    int32_t *vals, *perm;
+    unsigned long long* err_idx;
+    CK(s->alloc(&ru, G)); CK(s->alloc(&rv, G)); CK(s->alloc(&kk, G));
+    CK(s->alloc(&gu_c, G)); CK(s->alloc(&gv_c, G));
+    CK(s->alloc(&keys, G)); CK(s->alloc(&keys_s, G)); CK(s->alloc(&vals, G)); CK(s->alloc(&perm, G));
+    CK(s->alloc(&scratch, 8)); CK(s->alloc(&err_idx, 1));
+    const uint32_t init[8] = {0u, 0xffffffffu, 0u, 0xffffffffu, 0u, 0, 0, 0};  // err, min_u, max_u, min_v, max_v
+    CK(cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const unsigned long long big = ~0ull;
+    CK(cudaMemcpyAsync(err_idx, &big, sizeof(big), cudaMemcpyHostToDevice, st));
+    PrepIn pin{};
+    pin.x = din[0]; pin.y = din[1]; pin.z = din[2]; pin.sx = din[3]; pin.sy = din[4]; pin.sz = din[5];
+    pin.qw = din[6]; pin.qx = din[7]; pin.qy = din[8]; pin.qz = din[9]; pin.o = din[10];
+    pin.G = G;
+    for (int a = 0; a < 3; ++a) {
+      pin.c0[a] = F.center[a];
+      pin.au[a] = F.axis_u[a];
+      pin.av[a] = F.axis_v[a];
+    }
+    pin.rho = F.radius;
+    CK(launch_prep_raw(pin, ru, rv, kk, scratch, err_idx, scratch + 1, st));
+    uint32_t hs[8];
+    unsigned long long hbad;
+    CK(cudaMemcpyAsync(hs, scratch, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hbad, err_idx, sizeof(hbad), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hs[0] & 1u)
+      return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(hbad) +
+                                            " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
+                                            "SPEC.md:30-33)");
+    if (hs[0] & 2u) return fail(LOBE_E_INVALID_INPUT, "non-finite grid coordinate at " + std::to_string(hbad));
+    auto ord2f = [](uint32_t u) {
+      uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+      float f;
+      std::memcpy(&f, &b, 4);
+      return f;
+    };
+    s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
+    if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
+      return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
+    CK(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, keys, vals, st));
+    size_t tmpb = 0;
+    CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st));
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tmpb, st));
+    CK(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st));
+    CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
+    CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
+    CK(s->alloc(&s->o2, (size_t)s->G_pad));
+    CK(s->alloc(&s->gu, (size_t)s->G_pad));
+    CK(s->alloc(&s->gv, (size_t)s->G_pad));
+    CK(s->alloc(&s->iperm, (size_t)G));
+    CK(launch_pack(G, s->G_pad, perm, din[0], din[1], din[2], kk, din[10], gu_c, gv_c, s->xy, s->zk, s->o2, s->gu,
+                   s->gv, s->iperm, st));
+    cudaFreeAsync(tmp, st);
+    s->release(ru); s->release(rv); s->release(kk); s->release(gu_c); s->release(gv_c);
+    s->release(keys); s->release(keys_s); s->release(vals); s->release(perm); s->release(scratch);
+    s->release(err_idx);
+    if (dev_in) s->release(dev_in);
+
+    // ---- a2 camera setup (local shard) + camera-centre grid coords
+    std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
+    s->cam_gu.assign(s->N_loc, 0.f);
+    s->cam_gv.assign(s->N_loc, 0.f);
+    for (int64_t c = 0; c < s->N_loc; ++c) {
+      const lobe_camera& k = cams[s->cam_begin + c];
+      hset[c] = camera_setup(k);
+      double oc[3];
+      cam_centre(k, oc);
+      float ru_, rv_;
+      ground_uv_host((float)oc[0], (float)oc[1], (float)oc[2], F, &ru_, &rv_);
+      float a = (ru_ - s->mm[0]) / (s->mm[1] - s->mm[0]);
+      float b = (rv_ - s->mm[2]) / (s->mm[3] - s->mm[2]);
+      s->cam_gu[c] = std::fmin(1.0f, std::fmax(0.0f, a));
+      s->cam_gv[c] = std::fmin(1.0f, std::fmax(0.0f, b));
+    }
+    const int64_t NL = std::max<int64_t>(s->N_loc, 1);
+    CK(s->alloc(&s->cams, NL));
+    CK(s->alloc(&s->d_cam_gu, NL));
+    CK(s->alloc(&s->d_cam_gv, NL));
+    CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, st));
+    if (s->N_loc > 0) {
+      CK(cudaMemcpyAsync(s->d_cam_gu, s->cam_gu.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(s->d_cam_gv, s->cam_gv.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
+    }
+    // ---- a3/a4 visibility pass
+    CK(s->alloc(&s->rows, (size_t)NL * s->words));
+    CK(s->alloc(&s->flags, (size_t)s->n_tiles * NL));
+    CK(s->alloc(&s->part, (size_t)s->n_chunks * NL));
+    CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
+    CK(cudaEventRecord(s->ev[1], st));
+    if (s->N_loc > 0) {
+      VisArgs va{};
+      va.xy = reinterpret_cast<const float4*>(s->xy);
+      va.zk = reinterpret_cast<const float4*>(s->zk);
+      va.o2 = reinterpret_cast<const float2*>(s->o2);
+      va.cams = s->cams;
+      va.n_cams = s->N_loc;
+      va.n_chunks = s->n_chunks;
+      va.words = s->words;
+      va.rows = s->rows;
+      va.flags = s->flags;
+      va.part = s->part;
+      int grid = 0;
+      CK(launch_visibility(va, s->num_sms, st, &grid));
+    }
+    CK(cudaEventRecord(s->ev[2], st));
+    if (s->N_loc > 0) CK(launch_reduce_partials(s->part, s->n_chunks, s->N_loc, s->K, s->D, s->zmin, s->zmax, st));
+    // ---- (tile, camera) lists
+    CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
+    uint32_t* cnt;
+    CK(s->alloc(&cnt, (size_t)s->n_tiles + 1));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
+    if (s->N_loc > 0) CK(launch_tile_count(s->flags, s->n_tiles, s->N_loc, cnt, st));
+    size_t sb = 0;
+    CK(exclusive_scan_u32(nullptr, sb, cnt, s->tile_off, s->n_tiles + 1, st));
+    CK(cudaMallocAsync(&tmp, sb, st));
+    CK(exclusive_scan_u32(tmp, sb, cnt, s->tile_off, s->n_tiles + 1, st));
+    cudaFreeAsync(tmp, st);
+    s->release(cnt);
+    uint32_t np = 0;
+    CK(cudaMemcpyAsync(&np, s->tile_off + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    s->n_pairs = np;
+    CK(s->alloc(&s->pair_cam, (size_t)np));
+    CK(s->alloc(&s->pair_tile, (size_t)np));
+    if (s->N_loc > 0 && np > 0)
+      CK(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
+    // ---- evaluation scratch
+    CK(s->alloc(&s->zp, (size_t)s->G_pad));
+    CK(s->alloc(&s->word_zone, (size_t)s->words));
+    CK(s->alloc(&s->tile_zone, (size_t)s->n_tiles));
+    CK(s->alloc(&s->zp_count, (size_t)kMaxZones * kMaxZones));
+    CK(s->alloc(&s->dz, 1));
+    CK(s->alloc(&s->d_zp_cell, (size_t)kMaxZones * kMaxZones));
+    CK(s->alloc(&s->ncb, (size_t)NL * kMaxBlocks));
+    CK(s->alloc(&s->n0cb, (size_t)NL * kMaxBlocks));
+    CK(s->alloc(&s->member, NL)); CK(s->alloc(&s->sel, NL)); CK(s->alloc(&s->home, NL));
+    CK(s->alloc(&s->counts, 3 * kMaxBlocks));
+    CK(s->alloc(&s->incid, kMaxBlocks));
+    CK(cudaEventRecord(s->ev[3], st));
+    CK(cudaStreamSynchronize(st));
+    s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
+    s->st.t_vis_ms = ms_between(s->ev[1], s->ev[2]);
+    s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
+    s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
+    s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
+    s->st.bytes_written = (uint64_t)s->N_loc * (uint64_t)s->words * 4ull;
+    s->st.n_gaussians = G;
+    s->st.n_cameras = n_cams;
+    s->st.n_local_cameras = s->N_loc;
+    s->st.cam_begin = s->cam_begin;
+    s->st.tile_pairs = (uint64_t)np;
+    return LOBE_OK;
+  }();
+  if (rs != LOBE_OK) {
+    std::string keep = g_err;
+    lobe_free_scene(s);
+    g_err = keep;
+    return rs;
+  }
+  if (inout_frame) *inout_frame = F;
+  *out = s;
+  return LOBE_OK;
+}
+
+lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* K, double* depth_mean, float* z_min,
+                                float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member, int32_t* home) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  TRY(ensure_eval(s, g));
+  const size_t NL = (size_t)s->N_loc;
+  TRY(copy_out(s, K, s->K, NL * 4));
+  TRY(copy_out(s, depth_mean, s->D, NL * 8));
+  TRY(copy_out(s, z_min, s->zmin, NL * 4));
+  TRY(copy_out(s, z_max, s->zmax, NL * 4));
+  if (n_cb || n0_cb) {
+    // device layout is [c][B] with B = g.B stride
+    TRY(copy_out(s, n_cb, s->ncb, NL * g.B * 4));
+    TRY(copy_out(s, n0_cb, s->n0cb, NL * g.B * 4));
+  }
+  TRY(copy_out(s, member, s->member, NL * 8));
+  TRY(copy_out(s, home, s->home, NL * 4));
+  CK(cudaStreamSynchronize(s->stream));
+  return LOBE_OK;
+}
+
+lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_block_partial + lobe_masks_combine");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  TRY(ensure_eval(s, g));
+  uint64_t inc[kMaxBlocks];
+  for (int b = 0; b < g.B; ++b) inc[b] = s->h_incid[b];
+  fill_records(s, g, s->h_ncams, inc, s->h_gvis, out, objective);
+  return LOBE_OK;
+}
+
+lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_crop_from_masks on combined masks");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  TRY(ensure_eval(s, g));
+  return lobe_crop_from_masks(s, grid, s->masks, crop, eligible);
+}
+
+lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
+                                 uint64_t* eligible) {
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  // the zone tables on the device must describe this grid (evaluate() uploads them)
+  {
+    ZoneTables Z{};
+    build_axis(g.m, g.v, g.dv, &Z.U);
+    build_axis(g.n, g.h, g.dh, &Z.V);
+    if (s->hz.m != g.m || s->hz.n != g.n || std::memcmp(&Z.U, &s->hz.U, sizeof(AxisZones)) != 0 ||
+        std::memcmp(&Z.V, &s->hz.V, sizeof(AxisZones)) != 0) {
+      s->ev_valid = false;
+      TRY(evaluate(s, g, nullptr));
+    }
+  }
+  const int64_t W64 = (s->G + 63) / 64;
+  const size_t bytes = (size_t)g.B * W64 * 8;
+  uint32_t *dc = nullptr, *de = nullptr;
+  if (crop) CK(s->alloc(&dc, bytes / 4));
+  if (eligible) CK(s->alloc(&de, bytes / 4));
+  CK(cudaEventRecord(s->ev[5], s->stream));
+  CK(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, dc, de, s->stream));
+  CK(cudaEventRecord(s->ev[6], s->stream));
+  TRY(copy_out(s, crop, dc, bytes));
+  TRY(copy_out(s, eligible, de, bytes));
+  s->release(dc);
+  s->release(de);
+  CK(cudaStreamSynchronize(s->stream));
+  s->st.t_crop_ms = ms_between(s->ev[5], s->ev[6]);
+  return LOBE_OK;
+}
+
+lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
+                               uint64_t* incid) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (!d_masks) return fail(LOBE_E_INVALID_CONFIG, "d_masks NULL");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  s->ev_valid = false;  // masks go to the caller's buffer; do not cache
+  CK(cudaMemsetAsync(d_masks, 0, sizeof(uint32_t) * g.B * s->words, s->stream));
+  TRY(evaluate(s, g, d_masks));
+  if (n_cams) CK(cudaMemcpy(n_cams, s->h_ncams, sizeof(uint32_t) * g.B, cudaMemcpyDefault));
+  if (incid) CK(cudaMemcpy(incid, s->h_incid, sizeof(uint64_t) * g.B, cudaMemcpyDefault));
+  return LOBE_OK;
+}
+
+lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
+                               uint32_t* g_vis) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (B < 1 || B > kMaxBlocks || W < 1) return fail(LOBE_E_INVALID_CONFIG, "bad B or W");
+  CK(cudaSetDevice(s->device));
+  CK(cudaMemsetAsync(s->counts + kMaxBlocks, 0, sizeof(uint32_t) * kMaxBlocks, s->stream));
+  CK(cudaEventRecord(s->ev[5], s->stream));
+  CK(launch_masks_combine(d_gathered, W, B, s->words, d_out, s->counts + kMaxBlocks, s->stream));
+  CK(cudaEventRecord(s->ev[6], s->stream));
+  if (g_vis) CK(cudaMemcpyAsync(g_vis, s->counts + kMaxBlocks, sizeof(uint32_t) * B, cudaMemcpyDefault, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->st.t_comm_ms = ms_between(s->ev[5], s->ev[6]);
+  return LOBE_OK;
+}
+
+lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint32_t* n_cams, const uint64_t* incid,
+                               const uint32_t* g_vis, lobe_block_load* out, uint32_t* objective) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  GridV g;
+  TRY(check_grid(grid, &g));
+  if (!(s->hz.m == g.m && s->hz.n == g.n)) return fail(LOBE_E_STATE, "lobe_block_partial first");
+  fill_records(s, g, n_cams, incid, g_vis, out, objective);
+  return LOBE_OK;
+}
+
+lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t* rows) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (c0 < 0 || count < 0 || c0 + count > s->N_loc) return fail(LOBE_E_INVALID_INDEX, "camera range");
+  if (count == 0) return LOBE_OK;
+  CK(cudaSetDevice(s->device));
+  const size_t W32 = (size_t)((s->G + 31) / 32);
+  uint32_t* d = nullptr;
+  CK(s->alloc(&d, W32 * count));
+  CK(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, d, s->stream));
+  TRY(copy_out(s, rows, d, W32 * count * 4));
+  s->release(d);
+  CK(cudaStreamSynchronize(s->stream));
+  return LOBE_OK;
+}
+
+lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
+  if (!s || !out) return fail(LOBE_E_STATE, "NULL");
+  *out = s->st;
+  return LOBE_OK;
+}
+
+lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lobe_objective_fn objective, void* ctx,
+                        float* v_out, float* h_out, uint32_t* history, float* cut_history) {
+  g_err.clear();
+  if (m < 1 || n < 1 || m * n > kMaxBlocks) return fail(LOBE_E_INVALID_CONFIG, "grid m, n");
+  if (!objective) return fail(LOBE_E_INVALID_CONFIG, "objective NULL");
+  lobe_balance_opts o{100, 0, 0.1f, 0.15, 8};
+  if (opts) o = *opts;
+  if (o.L <= 0) o.L = 100;
+  if (o.n_sobol < 0) o.n_sobol = 8;
+  std::string err;
+  auto f = [&](const float* v, const float* h, uint32_t* val) { return objective(ctx, v, h, val); };
+  int rc = lobe::bo_run(m, n, o.L, o.seed, o.n_sobol, f, v_out, h_out, history, cut_history, &err);
+  if (rc != 0) return fail(LOBE_E_INVALID_CONFIG, "bo: " + err);
+  return LOBE_OK;
+}
+
+lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lobe_balance_opts* opts, float* v_out,
+                                   float* h_out, uint32_t* history, float* cut_history, lobe_block_load* best) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_bo_run with the exchange objective");
+  if (m < 1 || n < 1 || m * n > kMaxBlocks) return fail(LOBE_E_INVALID_CONFIG, "grid m, n");
+  lobe_balance_opts o{100, 0, 0.1f, 0.15, 8};
+  if (opts) o = *opts;
+  if (o.L <= 0) o.L = 100;
+  if (o.n_sobol < 0) o.n_sobol = 8;
+  const float ds = o.delta_scale > 0.0f ? o.delta_scale : 0.1f;
+  const double tau = o.tau < 0.0 ? 0.15 : o.tau;
+  const float dv = ds / (float)m, dh = ds / (float)n;  // ledger L14
+  lobe_status last = LOBE_OK;
+  auto f = [&](const float* v, const float* h, uint32_t* val) -> int {
+    lobe_grid gr{m, n, v, h, dv, dh, tau};
+    GridV g;
+    lobe_status st = check_grid(&gr, &g);
+    if (st == LOBE_OK) st = ensure_eval(s, g);
+    if (st != LOBE_OK) {
+      last = st;
+      return 1;
+    }
+    uint32_t b = 0;
+    for (int k = 0; k < g.B; ++k) b = std::max(b, s->h_gvis[k]);
+    *val = b;
+    return 0;
+  };
+  std::vector<float> vb(std::max(m - 1, 1)), hb(std::max(n - 1, 1));
+  std::string err;
+  int rc = lobe::bo_run(m, n, o.L, o.seed, o.n_sobol, f, vb.data(), hb.data(), history, cut_history, &err);
+  if (rc != 0) return last != LOBE_OK ? last : fail(LOBE_E_INVALID_CONFIG, "bo: " + err);
+  if (v_out) std::copy(vb.begin(), vb.begin() + (m - 1), v_out);
+  if (h_out) std::copy(hb.begin(), hb.begin() + (n - 1), h_out);
+  if (best) {
+    lobe_grid gr{m, n, vb.data(), hb.data(), dv, dh, tau};
+    uint32_t obj;
+    TRY(lobe_block_loads(s, &gr, best, &obj));
+  }
+  return LOBE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// lobe_bo.cpp -- load-balance-aware scene partition: Bayesian optimisation of
+// the grid cuts (§4.1; design choices of SPEC.md:453-502).
+//
+//   minimise  max_b G_vis^(b)(v, h)                     (Eq. 2)
+//   v_i in [ (v0_{i-1}+v0_i)/2, (v0_i+v0_{i+1})/2 ],    v0_i = i/m
+//   start at the uniform cuts, L = 100 evaluations, track the best
+//
+// The paper names only "BO with a GP surrogate" (Ax/BoTorch); the
+// concrete choices follow SPEC (ledger L20): 8 scrambled Sobol points after the
+// uniform cuts, then a GP with a Matern-5/2 ARD kernel fitted by maximising the
+// log marginal likelihood (multi-start coordinate search), expected improvement
+// maximised over 1024 quasi-random candidates refined by 20 pattern-search
+// steps. Proposals are rounded to fp32 before evaluation and the objective is
+// cached on the fp32 bit pattern (ledger L15); ties keep the earliest (L16).
+// The bounds are shrunk by 1e-6 so the cuts stay strictly increasing after fp32
+// rounding (ledger L23). Deterministic for a given seed. Host code: the loop is
+// sequential; each evaluation runs on the GPU (a5-a8).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace lobe {
+namespace {
+
+struct Rng {  // splitmix64
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed) {}
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double uniform() { return (next() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+// Sobol direction numbers (Joe & Kuo), dims 2..16: degree s, coefficient a, m_i.
+struct SobolDim {
+  int s, a;
+  int m[8];
+};
+const SobolDim kSobol[] = {
+    {1, 0, {1}},          {2, 1, {1, 3}},         {3, 1, {1, 3, 1}},      {3, 2, {1, 1, 1}},
+    {4, 1, {1, 1, 3, 3}}, {4, 4, {1, 3, 5, 13}},  {5, 2, {1, 1, 5, 5, 17}}, {5, 4, {1, 1, 5, 5, 5}},
+    {5, 7, {1, 1, 7, 11, 19}}, {5, 11, {1, 1, 5, 1, 1}}, {5, 13, {1, 1, 1, 3, 11}}, {5, 14, {1, 3, 5, 5, 31}},
+    {6, 1, {1, 3, 3, 9, 7, 49}}, {6, 13, {1, 1, 1, 15, 21, 21}}, {6, 16, {1, 3, 1, 13, 27, 49}},
+};
+
+class Sobol {
+ public:
+  Sobol(int D, uint64_t seed) : D_(D), V_(D, std::vector<uint32_t>(32)), x_(D, 0u), shift_(D), idx_(0) {
+    for (int k = 0; k < 32; ++k) V_[0][k] = 1u << (31 - k);
+    for (int d = 1; d < D; ++d) {
+      const SobolDim& sd = kSobol[(d - 1) % 15];
+      const int s = sd.s;
+      for (int k = 0; k < s && k < 32; ++k) V_[d][k] = (uint32_t)sd.m[k] << (31 - k);
+      for (int k = s; k < 32; ++k) {
+        uint32_t v = V_[d][k - s] ^ (V_[d][k - s] >> s);
+        for (int r = 1; r < s; ++r)
+          if ((sd.a >> (s - 1 - r)) & 1) v ^= V_[d][k - r];
+        V_[d][k] = v;
+      }
+    }
+    Rng r(seed ^ 0x5b0b01ull);
+    for (int d = 0; d < D; ++d) shift_[d] = (uint32_t)(r.next() >> 32);  // digital shift scrambling
+  }
+  void next(double* out) {
+    // Gray-code update, skipping the all-zero first point
+    ++idx_;
+    int c = __builtin_ctzll(idx_);
+    for (int d = 0; d < D_; ++d) {
+      x_[d] ^= V_[d][c];
+      out[d] = ((x_[d] ^ shift_[d]) + 0.5) / 4294967296.0;
+    }
+  }
+
+ private:
+  int D_;
+  std::vector<std::vector<uint32_t>> V_;
+  std::vector<uint32_t> x_, shift_;
+  uint64_t idx_;
+};
+
+// ------------------------------------------------------------------ GP
+struct GP {
+  int D = 0, n = 0;
+  std::vector<double> X, y;  // n x D inputs in [0,1], standardized targets
+  std::vector<double> ls;    // length scales
+  double sf2 = 1.0, noise = 1e-6;
+  std::vector<double> Lc, alpha;
+  double mean = 0, scale = 1;
+
+  double kern(const double* a, const double* b) const {
+    double r2 = 0;
+    for (int d = 0; d < D; ++d) {
+      const double t = (a[d] - b[d]) / ls[d];
+      r2 += t * t;
+    }
+    const double r = std::sqrt(5.0 * r2);
+    return sf2 * (1.0 + r + r * r / 3.0) * std::exp(-r);  // Matern-5/2
+  }
+  // Cholesky of K + noise I; returns false if not PD
+  bool factor(double nz) {
+    Lc.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double s = kern(&X[(size_t)i * D], &X[(size_t)j * D]) + (i == j ? nz : 0.0);
+        for (int k = 0; k < j; ++k) s -= Lc[(size_t)i * n + k] * Lc[(size_t)j * n + k];
+        if (i == j) {
+          if (!(s > 0)) return false;
+          Lc[(size_t)i * n + i] = std::sqrt(s);
+        } else {
+          Lc[(size_t)i * n + j] = s / Lc[(size_t)j * n + j];
+        }
+      }
+    return true;
+  }
+  void solve_lower(const std::vector<double>& b, std::vector<double>& x) const {
+    x.resize(n);
+    for (int i = 0; i < n; ++i) {
+      double s = b[i];
+      for (int k = 0; k < i; ++k) s -= Lc[(size_t)i * n + k] * x[k];
+      x[i] = s / Lc[(size_t)i * n + i];
+    }
+  }
+  void solve_upper(const std::vector<double>& b, std::vector<double>& x) const {
+    x.resize(n);
+    for (int i = n - 1; i >= 0; --i) {
+      double s = b[i];
+      for (int k = i + 1; k < n; ++k) s -= Lc[(size_t)k * n + i] * x[k];
+      x[i] = s / Lc[(size_t)i * n + i];
+    }
+  }
+  // factor with jitter escalation (x10 up to 1e-2)
+  bool refactor() {
+    for (double nz = noise; nz <= 1e-2 * 1.0001; nz *= 10.0)
+      if (factor(nz)) {
+        noise = nz;
+        std::vector<double> t;
+        solve_lower(y, t);
+        solve_upper(t, alpha);
+        return true;
+      }
+    return false;
+  }
+  double lml() {  // log marginal likelihood (up to a constant)
+    if (!refactor()) return -1e300;
+    double q = 0, ld = 0;
+    for (int i = 0; i < n; ++i) {
+      q += y[i] * alpha[i];
+      ld += std::log(Lc[(size_t)i * n + i]);
+    }
+    return -0.5 * q - ld;
+  }
+  void fit() {
+    // multi-start coordinate search over log length scales and log signal variance
+    const double starts[3] = {0.2, 0.5, 1.0};
+    double best = -1e301;
+    std::vector<double> best_ls(D, 0.5);
+    double best_sf = 1.0;
+    for (double s0 : starts) {
+      ls.assign(D, s0);
+      sf2 = 1.0;
+      noise = 1e-6;
+      double cur = lml();
+      double step = 2.0;
+      for (int sweep = 0; sweep < 4; ++sweep) {
+        bool improved = false;
+        for (int d = 0; d <= D; ++d) {
+          for (double f : {step, 1.0 / step}) {
+            double* p = (d < D) ? &ls[d] : &sf2;
+            const double old = *p;
+            const double nv = std::min(std::max(old * f, d < D ? 0.01 : 0.05), d < D ? 10.0 : 20.0);
+            if (nv == old) continue;
+            *p = nv;
+            noise = 1e-6;
+            const double v = lml();
+            if (v > cur + 1e-12) {
+              cur = v;
+              improved = true;
+            } else {
+              *p = old;
+            }
+          }
+        }
+        if (!improved) step = std::sqrt(step);
+      }
+      if (cur > best) {
+        best = cur;
+        best_ls = ls;
+        best_sf = sf2;
+      }
+    }
+    ls = best_ls;
+    sf2 = best_sf;
+    noise = 1e-6;
+    refactor();
+  }
+  void predict(const double* x, double* mu, double* sd) const {
+    std::vector<double> k(n), v;
+    for (int i = 0; i < n; ++i) k[i] = kern(x, &X[(size_t)i * D]);
+    double m = 0;
+    for (int i = 0; i < n; ++i) m += k[i] * alpha[i];
+    solve_lower(k, v);
+    double var = sf2;
+    for (int i = 0; i < n; ++i) var -= v[i] * v[i];
+    *mu = m;
+    *sd = std::sqrt(std::max(var, 0.0));
+  }
+};
+
+double norm_pdf(double z) { return 0.3989422804014327 * std::exp(-0.5 * z * z); }
+double norm_cdf(double z) { return 0.5 * std::erfc(-z / std::sqrt(2.0)); }
+
+// EI for minimisation: (best - mu) Phi(z) + sigma phi(z)
+double ei(double mu, double sd, double best) {
+  if (!(sd > 1e-12)) return std::max(best - mu, 0.0);
+  const double z = (best - mu) / sd;
+  return (best - mu) * norm_cdf(z) + sd * norm_pdf(z);
+}
+
+}  // namespace
+
+int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
+           const std::function<int(const float*, const float*, uint32_t*)>& objective, float* v_out, float* h_out,
+           uint32_t* history, float* cut_history, std::string* err) {
+  const int Dv = m - 1, Dh = n - 1, D = Dv + Dh;
+  // bounds in cut space: each cut moves at most halfway to its uniform neighbours
+  std::vector<double> lo(D), hi(D);
+  for (int i = 1; i <= Dv; ++i) {
+    lo[i - 1] = (2.0 * i - 1.0) / (2.0 * m) + 1e-6;
+    hi[i - 1] = (2.0 * i + 1.0) / (2.0 * m) - 1e-6;
+  }
+  for (int j = 1; j <= Dh; ++j) {
+    lo[Dv + j - 1] = (2.0 * j - 1.0) / (2.0 * n) + 1e-6;
+    hi[Dv + j - 1] = (2.0 * j + 1.0) / (2.0 * n) - 1e-6;
+  }
+  std::map<std::vector<uint32_t>, uint32_t> cache;
+  std::vector<std::vector<double>> Xs;  // normalised inputs
+  std::vector<double> ys;
+  std::vector<float> cuts(std::max(D, 1));
+  std::vector<float> best_cuts(std::max(D, 1));
+  uint32_t best_y = 0xffffffffu;
+
+  auto to_cuts = [&](const std::vector<double>& x) {
+    for (int d = 0; d < D; ++d) cuts[d] = (float)(lo[d] + std::min(std::max(x[d], 0.0), 1.0) * (hi[d] - lo[d]));
+  };
+  auto evaluate = [&](int l, std::vector<double> x, bool from_cuts) -> int {
+    if (!from_cuts) to_cuts(x);
+    std::vector<uint32_t> key(D);
+    for (int d = 0; d < D; ++d) std::memcpy(&key[d], &cuts[d], 4);
+    uint32_t val;
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      val = it->second;
+    } else {
+      if (objective(cuts.data(), cuts.data() + Dv, &val) != 0) {
+        *err = "objective failed at iteration " + std::to_string(l);
+        return 1;
+      }
+      cache[key] = val;
+    }
+    for (int d = 0; d < D; ++d) x[d] = (hi[d] > lo[d]) ? ((double)cuts[d] - lo[d]) / (hi[d] - lo[d]) : 0.5;
+    Xs.push_back(x);
+    ys.push_back((double)val);
+    if (history) history[l] = val;
+    if (cut_history)
+      for (int d = 0; d < D; ++d) cut_history[(size_t)l * D + d] = cuts[d];
+    if (val < best_y) {  // strict: ties keep the earliest (L16)
+      best_y = val;
+      best_cuts = cuts;
+    }
+    return 0;
+  };
+
+  // iteration 0: the uniform cuts (i/m, j/n) in fp32
+  for (int i = 1; i <= Dv; ++i) cuts[i - 1] = (float)((double)i / m);
+  for (int j = 1; j <= Dh; ++j) cuts[Dv + j - 1] = (float)((double)j / n);
+  if (evaluate(0, std::vector<double>(D, 0.5), true)) return 1;
+  Sobol sob(std::max(D, 1), seed);
+  std::vector<double> x(std::max(D, 1));
+  for (int l = 1; l < L; ++l) {
+    if (D == 0) {
+      if (evaluate(l, {}, true)) return 1;
+      continue;
+    }
+    if (l <= n_sobol) {
+      sob.next(x.data());
+      if (evaluate(l, std::vector<double>(x.begin(), x.begin() + D), false)) return 1;
+      continue;
+    }
+    // GP on standardized targets
+    GP gp;
+    gp.D = D;
+    gp.n = (int)Xs.size();
+    gp.X.resize((size_t)gp.n * D);
+    for (int i = 0; i < gp.n; ++i)
+      for (int d = 0; d < D; ++d) gp.X[(size_t)i * D + d] = Xs[i][d];
+    double mean = 0;
+    for (double v : ys) mean += v;
+    mean /= gp.n;
+    double var = 0;
+    for (double v : ys) var += (v - mean) * (v - mean);
+    double sd = std::sqrt(var / gp.n);
+    if (!(sd > 0)) sd = 1.0;
+    gp.y.resize(gp.n);
+    for (int i = 0; i < gp.n; ++i) gp.y[i] = (ys[i] - mean) / sd;
+    gp.fit();
+    const double best_s = ((double)best_y - mean) / sd;
+    // EI over 1024 quasi-random candidates (seeded) + 20 pattern-search steps
+    Rng rng(seed * 0x9E3779B97F4A7C15ull + (uint64_t)l);
+    std::vector<double> bx(D), cand(D);
+    double bei = -1.0;
+    for (int k = 0; k < 1024; ++k) {
+      for (int d = 0; d < D; ++d) cand[d] = rng.uniform();
+      double mu, s;
+      gp.predict(cand.data(), &mu, &s);
+      const double e = ei(mu, s, best_s);
+      if (e > bei) {
+        bei = e;
+        bx = cand;
+      }
+    }
+    double step = 0.1;
+    for (int it = 0; it < 20; ++it) {
+      bool moved = false;
+      std::vector<double> bestn = bx;
+      double beste = bei;
+      for (int d = 0; d < D; ++d)
+        for (double sgn : {1.0, -1.0}) {
+          cand = bx;
+          cand[d] = std::min(std::max(cand[d] + sgn * step, 0.0), 1.0);
+          double mu, s;
+          gp.predict(cand.data(), &mu, &s);
+          const double e = ei(mu, s, best_s);
+          if (e > beste) {
+            beste = e;
+            bestn = cand;
+            moved = true;
+          }
+        }
+      if (moved) {
+        bx = bestn;
+        bei = beste;
+      } else {
+        step *= 0.5;
+      }
+    }
+    if (evaluate(l, bx, false)) return 1;
+  }
+  for (int i = 0; i < Dv; ++i) v_out[i] = best_cuts[i];
+  for (int j = 0; j < Dh; ++j) h_out[j] = best_cuts[Dv + j];
+  return 0;
+}
+
+}  // namespace lobe

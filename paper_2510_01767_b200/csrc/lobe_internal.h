@@ -1,0 +1,139 @@
+// lobe_internal.h -- internal types shared by the host runtime (lobe_api.cpp)
+// and the sm_100a kernels (lobe_kernels.cu). Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lobe {
+
+// Geometry of the internal layout.
+constexpr int kTile = 1024;                 // Gaussians per smem stage / per row tile (32 u32 words)
+constexpr int kTileWords = kTile / 32;      // 32
+constexpr int kChunk = 16384;               // Gaussians per visibility work item (fixed: world-size invariance)
+constexpr int kTilesPerChunk = kChunk / kTile;
+constexpr int kMaxBlocks = 64;              // B <= 64 (member mask is one u64)
+constexpr int kMaxZones = 4 * kMaxBlocks + 2;  // per-axis zones upper bound
+constexpr uint16_t kMixed = 0xFFFF;
+
+// Per-camera projection rows: 16 floats, 64 B.
+struct __align__(16) CamSetup {
+  float Au[4];  // Au[0..2], au
+  float Av[4];  // Av[0..2], av
+  float Aw[4];  // Aw[0..2], aw
+  float Wf, Hf, zn, zf;
+};
+static_assert(sizeof(CamSetup) == 64, "CamSetup layout");
+
+// Per (chunk, camera) partial depth statistics written by the visibility kernel.
+struct __align__(16) VisPartial {
+  double S, O;       // sum o*w, sum o over visible Gaussians of the chunk
+  float zmin, zmax;  // min/max w
+  uint32_t K, pad;
+};
+static_assert(sizeof(VisPartial) == 32, "VisPartial layout");
+
+// Zone tables for one grid (a5): per axis, sorted breakpoints P[0..nz-2] with
+// P[0] = 0; zone z < nz-1 is [P[z], P[z+1]) (P[nz-1] := 1), zone nz-1 is {1}.
+struct AxisZones {
+  int nz;                      // number of zones including the top zone {1}
+  int count;                   // intervals on this axis (m or n)
+  float P[kMaxZones];          // breakpoints (nz-1 of them)
+  uint8_t cell[kMaxZones];     // delta=0 interval of the zone
+  uint64_t encl[kMaxZones];    // bitmask of enlarged intervals containing the zone
+};
+struct ZoneTables {
+  AxisZones U, V;
+  int m, n, B;
+};
+
+// ---- kernel launchers (lobe_kernels.cu) ------------------------------------
+struct PrepIn {
+  const float *x, *y, *z, *sx, *sy, *sz, *qw, *qx, *qy, *qz, *o;
+  int64_t G;
+  float c0[3], rho, au[3], av[3];
+};
+// Validation + per-Gaussian raw ground coords and footprint radius. err[0] =
+// error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
+cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* err,
+                            unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
+// Normalise to [0,1], Morton key, identity values.
+cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, float* gu, float* gv,
+                             uint32_t* keys, int32_t* vals, cudaStream_t st);
+cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                             int32_t* vout, int64_t n, cudaStream_t st);
+// Gather into the internal pair-interleaved layout, build the inverse permutation.
+cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float* x, const float* y,
+                        const float* z, const float* kk, const float* o, const float* gu_c, const float* gv_c,
+                        float* xy, float* zk, float* o2, float* gu, float* gv, int32_t* iperm, cudaStream_t st);
+
+// a3: visibility tests -> rows, tile flags, per-(chunk,camera) partials.
+struct VisArgs {
+  const float4* xy;
+  const float4* zk;
+  const float2* o2;
+  const CamSetup* cams;
+  int64_t n_cams;      // local cameras
+  int64_t n_chunks;
+  int64_t words;       // row stride in u32 words (G_pad / 32)
+  uint32_t* rows;
+  uint8_t* flags;      // [n_tiles x n_cams]
+  VisPartial* part;    // [n_chunks x n_cams]
+};
+cudaError_t launch_visibility(const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
+// a4: reduce partials in chunk order -> K, D, zmin, zmax.
+cudaError_t launch_reduce_partials(const VisPartial* part, int64_t n_chunks, int64_t n_cams, uint32_t* K, double* D,
+                                   float* zmin, float* zmax, cudaStream_t st);
+// tile -> camera lists (CSR) from flags.
+cudaError_t launch_tile_count(const uint8_t* flags, int64_t n_tiles, int64_t n_cams, uint32_t* counts,
+                              cudaStream_t st);
+cudaError_t exclusive_scan_u32(void* tmp, size_t& tmp_bytes, const uint32_t* in, uint32_t* out, int64_t n,
+                               cudaStream_t st);
+cudaError_t launch_tile_fill(const uint8_t* flags, int64_t n_tiles, int64_t n_cams, const uint32_t* offsets,
+                             uint32_t* pair_cam, uint32_t* pair_tile, cudaStream_t st);
+
+// a5: per-Gaussian zone pair, per-word / per-tile uniform zone, per-zone counts.
+cudaError_t launch_zones(const ZoneTables* dz, int nzv, int64_t G, int64_t G_pad, const float* gu, const float* gv,
+                         uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone, uint32_t* zp_count,
+                         cudaStream_t st);
+// a6: zone-pair histograms per camera from the (tile, camera) pairs.
+cudaError_t launch_hist(int64_t n_pairs, const uint32_t* pair_cam, const uint32_t* pair_tile, const uint32_t* rows,
+                        int64_t words, const uint16_t* zp, const uint16_t* word_zone, const uint16_t* tile_zone,
+                        int nzp, uint32_t* hist, cudaStream_t st);
+// a7: n, n0, member, home, selection mask, |C^(b)|, I_b.
+struct AssignArgs {
+  const ZoneTables* dz;
+  const uint32_t* hist;
+  int nzp;
+  const uint32_t* K;
+  const float* cam_gu;
+  const float* cam_gv;
+  int64_t n_cams;
+  double tau;
+  int mode;
+  uint32_t* ncb;
+  uint32_t* n0cb;
+  uint64_t* member;
+  int32_t* home;
+  uint64_t* sel;
+  uint32_t* ncams;       // [B]
+  unsigned long long* incid;  // [B]
+};
+cudaError_t launch_assign(const AssignArgs& a, cudaStream_t st);
+// a8: per-block OR of selected rows -> masks (internal order) + popcounts.
+cudaError_t launch_block_masks(int64_t n_tiles, const uint32_t* tile_off, const uint32_t* pair_cam,
+                               const uint64_t* sel, const uint32_t* rows, int64_t words, int B, uint32_t* masks,
+                               uint32_t* gvis, cudaStream_t st);
+cudaError_t launch_masks_combine(const uint32_t* gathered, int W, int B, int64_t words, uint32_t* out,
+                                 uint32_t* gvis, cudaStream_t st);
+// a9: caller-order crop / eligible masks.
+cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint8_t* zp_cellblock,
+                        const uint32_t* masks, int64_t words, int B, uint32_t* crop32, uint32_t* elig32,
+                        cudaStream_t st);
+cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
+                               int64_t count, uint32_t* out, cudaStream_t st);
+// G_blk from per-zone-pair counts.
+cudaError_t launch_gblk(const ZoneTables* dz, int nzv, int nzp, const uint32_t* zp_count, uint32_t* gblk,
+                        cudaStream_t st);
+
+}  // namespace lobe

@@ -1,0 +1,367 @@
+"""ctypes binding of the C ABI in include/lobe.h (argument marshalling only).
+
+Every step of the path runs in csrc/liblobe.so (sm_100a kernels + host
+runtime). There is no fallback: if the library is missing or no CUDA device is
+present, calls raise. Names follow the C ABI without the `lobe_` prefix.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "liblobe.so")
+
+STATUS = {0: "OK", 1: "INVALID_INPUT", 2: "INVALID_CONFIG", 3: "INVALID_CUTS", 4: "INVALID_INDEX",
+          5: "DEGENERATE_SCENE", 6: "CUDA", 7: "NCCL", 8: "OOM", 9: "STATE"}
+ASSIGN_RATIO, ASSIGN_HOME, ASSIGN_UNION = 0, 1, 2
+FRAME_AUTO_CENTER, FRAME_AUTO_RADIUS, FRAME_AUTO_AXES, FRAME_AUTO_ALL = 1, 2, 4, 7
+
+# symbols include/lobe.h declares (tests check the library exports all of them)
+EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign_cameras", "lobe_block_loads",
+           "lobe_crop_masks", "lobe_balance_partition", "lobe_bo_run", "lobe_mask_words", "lobe_block_partial",
+           "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
+           "lobe_get_stats", "lobe_version"]
+
+
+class LobeError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class Gaussians(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64)] + [(k, ctypes.c_void_p) for k in
+                                           ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")] + \
+               [("on_device", ctypes.c_int32)]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("fx", ctypes.c_float), ("fy", ctypes.c_float), ("cx", ctypes.c_float),
+                ("cy", ctypes.c_float), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("R", ctypes.c_float * 9), ("t", ctypes.c_float * 3), ("z_near", ctypes.c_float),
+                ("z_far", ctypes.c_float)]
+
+
+class Frame(ctypes.Structure):
+    _fields_ = [("center", ctypes.c_float * 3), ("radius", ctypes.c_float), ("axis_u", ctypes.c_float * 3),
+                ("axis_v", ctypes.c_float * 3), ("auto_flags", ctypes.c_uint32)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("assign_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("n", ctypes.c_int32), ("v", ctypes.c_void_p), ("h", ctypes.c_void_p),
+                ("delta_v", ctypes.c_float), ("delta_h", ctypes.c_float), ("tau", ctypes.c_double)]
+
+
+class BlockLoad(ctypes.Structure):
+    _fields_ = [("block_id", ctypes.c_int32), ("row", ctypes.c_int32), ("col", ctypes.c_int32),
+                ("lo", ctypes.c_float * 2), ("hi", ctypes.c_float * 2), ("area", ctypes.c_double),
+                ("n_cams", ctypes.c_uint32), ("g_blk", ctypes.c_uint32), ("g_vis", ctypes.c_uint32),
+                ("g_avgvis", ctypes.c_double), ("incidences", ctypes.c_uint64)]
+
+
+class BalanceOpts(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int32), ("seed", ctypes.c_uint64), ("delta_scale", ctypes.c_float),
+                ("tau", ctypes.c_double), ("n_sobol", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("t_prep_ms", "t_vis_ms", "t_hist_ms", "t_loads_ms", "t_comm_ms",
+                                               "t_crop_ms")] + \
+               [(k, ctypes.c_uint64) for k in ("tests_executed", "bytes_read", "bytes_written", "vis_launches",
+                                               "evaluations")] + \
+               [(k, ctypes.c_int64) for k in ("n_gaussians", "n_cameras", "n_local_cameras", "cam_begin")] + \
+               [("tile_pairs", ctypes.c_uint64)]
+
+
+OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
+                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_uint32))
+
+_lib = None
+
+
+def lib():
+    """Load csrc/liblobe.so. Raises if it is missing: there is no CPU path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2510_01767_b200.build` "
+                              "(the engine has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.lobe_last_error.restype = ctypes.c_char_p
+        L.lobe_version.restype = ctypes.c_char_p
+        L.lobe_mask_words.restype = ctypes.c_size_t
+        L.lobe_mask_words.argtypes = [vp]
+        L.lobe_free_scene.argtypes = [vp]
+        L.lobe_free_scene.restype = None
+        L.lobe_load_scene.argtypes = [ctypes.POINTER(Gaussians), ctypes.POINTER(Camera), i64,
+                                      ctypes.POINTER(Frame), ctypes.POINTER(Options), ctypes.POINTER(vp)]
+        L.lobe_assign_cameras.argtypes = [vp, ctypes.POINTER(Grid)] + [vp] * 8
+        L.lobe_block_loads.argtypes = [vp, ctypes.POINTER(Grid), vp, vp]
+        L.lobe_crop_masks.argtypes = [vp, ctypes.POINTER(Grid), vp, vp]
+        L.lobe_balance_partition.argtypes = [vp, i32, i32, ctypes.POINTER(BalanceOpts), vp, vp, vp, vp, vp]
+        L.lobe_bo_run.argtypes = [i32, i32, ctypes.POINTER(BalanceOpts), OBJECTIVE_FN, vp, vp, vp, vp, vp]
+        L.lobe_block_partial.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
+        L.lobe_masks_combine.argtypes = [vp, i32, vp, i32, vp, vp]
+        L.lobe_block_records.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp, vp, vp]
+        L.lobe_crop_from_masks.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
+        L.lobe_export_rows.argtypes = [vp, i64, i64, vp]
+        L.lobe_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+        for name in EXPORTS:
+            if name not in ("lobe_last_error", "lobe_version", "lobe_mask_words", "lobe_free_scene"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        raise LobeError(code, lib().lobe_last_error().decode())
+
+
+def _ptr(a):
+    """Address of a numpy array or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous()
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(type(a))
+
+
+def version():
+    return lib().lobe_version().decode()
+
+
+def make_cameras(scene):
+    N = scene.N
+    arr = (Camera * N)()
+    R = scene.R.reshape(N, 9)
+    for c in range(N):
+        k = arr[c]
+        k.id = int(scene.cam_id[c])
+        k.fx, k.fy, k.cx, k.cy = float(scene.fx[c]), float(scene.fy[c]), float(scene.cx[c]), float(scene.cy[c])
+        k.width, k.height = int(scene.width[c]), int(scene.height[c])
+        k.R[:] = [float(v) for v in R[c]]
+        k.t[:] = [float(v) for v in scene.t[c]]
+        k.z_near, k.z_far = float(scene.z_near[c]), float(scene.z_far[c])
+    return arr
+
+
+def make_grid(m, n, v=None, h=None, delta_v=-1.0, delta_h=-1.0, tau=-1.0):
+    """Grid struct + the arrays it points to (kept alive in the returned tuple)."""
+    v = np.ascontiguousarray(v if v is not None else [np.float32(i / m) for i in range(1, m)], np.float32)
+    h = np.ascontiguousarray(h if h is not None else [np.float32(j / n) for j in range(1, n)], np.float32)
+    g = Grid(int(m), int(n), v.ctypes.data if v.size else None, h.ctypes.data if h.size else None,
+             float(delta_v), float(delta_h), float(tau))
+    return g, (v, h)
+
+
+class Scene:
+    """Owning wrapper of a lobe_scene* handle."""
+
+    def __init__(self, gaussians, cameras, frame=None, device=0, rank=0, world=1, stream=None,
+                 assign_mode=ASSIGN_RATIO):
+        """gaussians: an object with x..opacity attributes (numpy host arrays or
+        torch CUDA tensors); cameras: a synth Scene (its camera arrays) or a
+        ctypes Camera array. frame: dict(center, radius, axis_u, axis_v) or None
+        (automatic, ledger L12)."""
+        L = lib()
+        self._keep = []
+        names = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
+        arrs = [getattr(gaussians, k) for k in names]
+        on_dev = int(not isinstance(arrs[0], np.ndarray))
+        if not on_dev:
+            arrs = [np.ascontiguousarray(a, np.float32) for a in arrs]
+        self._keep.append(arrs)
+        g = Gaussians(int(arrs[0].shape[0]), *[_ptr(a) for a in arrs], on_dev)
+        cams = cameras if isinstance(cameras, ctypes.Array) else make_cameras(cameras)
+        fr = Frame()
+        flags = 0
+        frame = frame or {}
+        if frame.get("center") is None:
+            flags |= FRAME_AUTO_CENTER
+        else:
+            fr.center[:] = [float(v) for v in frame["center"]]
+        if frame.get("radius") is None:
+            flags |= FRAME_AUTO_RADIUS
+        else:
+            fr.radius = float(frame["radius"])
+        if frame.get("axis_u") is None:
+            flags |= FRAME_AUTO_AXES
+        else:
+            fr.axis_u[:] = [float(v) for v in frame["axis_u"]]
+            fr.axis_v[:] = [float(v) for v in frame["axis_v"]]
+        fr.auto_flags = flags
+        st = stream if (stream is None or isinstance(stream, int)) else stream.cuda_stream
+        opt = Options(int(device), int(rank), int(world), st, int(assign_mode), 0)
+        h = ctypes.c_void_p()
+        _check(L.lobe_load_scene(ctypes.byref(g), cams, len(cams), ctypes.byref(fr), ctypes.byref(opt),
+                                 ctypes.byref(h)))
+        self.handle = h
+        self.frame = dict(center=np.array(fr.center[:], np.float32), radius=np.float32(fr.radius),
+                          axis_u=np.array(fr.axis_u[:], np.float32), axis_v=np.array(fr.axis_v[:], np.float32))
+        s = self.stats()
+        self.G, self.N, self.n_local, self.cam_begin = s.n_gaussians, s.n_cameras, s.n_local_cameras, s.cam_begin
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().lobe_free_scene(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- calls ----------------------------------------------------------
+    def stats(self):
+        s = Stats()
+        _check(lib().lobe_get_stats(self.handle, ctypes.byref(s)))
+        return s
+
+    def assign_cameras(self, m, n, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        NL, B = self.n_local, m * n
+        out = dict(K=np.empty(NL, np.uint32), D=np.empty(NL, np.float64), zmin=np.empty(NL, np.float32),
+                   zmax=np.empty(NL, np.float32), n=np.empty((NL, B), np.uint32), n0=np.empty((NL, B), np.uint32),
+                   member=np.empty(NL, np.uint64), home=np.empty(NL, np.int32))
+        _check(lib().lobe_assign_cameras(self.handle, ctypes.byref(g), *[_ptr(out[k]) for k in
+                                                                         ("K", "D", "zmin", "zmax", "n", "n0",
+                                                                          "member", "home")]))
+        return out
+
+    def block_loads(self, m, n, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        recs = (BlockLoad * (m * n))()
+        obj = ctypes.c_uint32()
+        _check(lib().lobe_block_loads(self.handle, ctypes.byref(g), recs, ctypes.byref(obj)))
+        return records_to_dict(recs, int(obj.value))
+
+    def crop_masks(self, m, n, crop=True, eligible=True, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        W = (self.G + 63) // 64
+        c = np.empty((m * n, W), np.uint64) if crop else None
+        e = np.empty((m * n, W), np.uint64) if eligible else None
+        _check(lib().lobe_crop_masks(self.handle, ctypes.byref(g), _ptr(c), _ptr(e)))
+        return c, e
+
+    def crop_masks_into(self, m, n, crop_ptr, elig_ptr, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        _check(lib().lobe_crop_masks(self.handle, ctypes.byref(g), crop_ptr, elig_ptr))
+
+    def balance_partition(self, m, n, L=100, seed=0, delta_scale=0.1, tau=0.15, n_sobol=8):
+        o = BalanceOpts(int(L), int(seed), float(delta_scale), float(tau), int(n_sobol))
+        v = np.empty(max(m - 1, 1), np.float32)
+        h = np.empty(max(n - 1, 1), np.float32)
+        hist = np.empty(L, np.uint32)
+        D = (m - 1) + (n - 1)
+        ch = np.empty((L, max(D, 1)), np.float32)
+        recs = (BlockLoad * (m * n))()
+        _check(lib().lobe_balance_partition(self.handle, m, n, ctypes.byref(o), _ptr(v), _ptr(h), _ptr(hist),
+                                            _ptr(ch), recs))
+        return dict(v=v[:m - 1], h=h[:n - 1], history=hist, cut_history=ch[:, :D], best=records_to_dict(recs, None))
+
+    def export_rows(self, c0=0, count=None):
+        count = self.n_local - c0 if count is None else count
+        out = np.empty((count, (self.G + 31) // 32), np.uint32)
+        _check(lib().lobe_export_rows(self.handle, int(c0), int(count), _ptr(out)))
+        return out
+
+    def mask_words(self):
+        return int(lib().lobe_mask_words(self.handle))
+
+    def block_partial(self, m, n, d_masks, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        B = m * n
+        nc = np.empty(B, np.uint32)
+        inc = np.empty(B, np.uint64)
+        _check(lib().lobe_block_partial(self.handle, ctypes.byref(g), _ptr(d_masks), _ptr(nc), _ptr(inc)))
+        return nc, inc
+
+    def masks_combine(self, B, d_gathered, W, d_out):
+        gv = np.empty(B, np.uint32)
+        _check(lib().lobe_masks_combine(self.handle, int(B), _ptr(d_gathered), int(W), _ptr(d_out), _ptr(gv)))
+        return gv
+
+    def block_records(self, m, n, n_cams, incid, g_vis, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        recs = (BlockLoad * (m * n))()
+        obj = ctypes.c_uint32()
+        n_cams = np.ascontiguousarray(n_cams, np.uint32)
+        incid = np.ascontiguousarray(incid, np.uint64)
+        g_vis = np.ascontiguousarray(g_vis, np.uint32)
+        _check(lib().lobe_block_records(self.handle, ctypes.byref(g), _ptr(n_cams), _ptr(incid), _ptr(g_vis), recs,
+                                        ctypes.byref(obj)))
+        return records_to_dict(recs, int(obj.value))
+
+    def crop_from_masks(self, m, n, d_masks, crop=True, eligible=True, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        W = (self.G + 63) // 64
+        c = np.empty((m * n, W), np.uint64) if crop else None
+        e = np.empty((m * n, W), np.uint64) if eligible else None
+        _check(lib().lobe_crop_from_masks(self.handle, ctypes.byref(g), _ptr(d_masks), _ptr(c), _ptr(e)))
+        return c, e
+
+
+def records_to_dict(recs, objective):
+    B = len(recs)
+    out = dict(block_id=np.array([r.block_id for r in recs], np.int32),
+               n_cams=np.array([r.n_cams for r in recs], np.uint32),
+               g_blk=np.array([r.g_blk for r in recs], np.uint32),
+               g_vis=np.array([r.g_vis for r in recs], np.uint32),
+               incidences=np.array([r.incidences for r in recs], np.uint64),
+               area=np.array([r.area for r in recs], np.float64),
+               g_avgvis=np.array([r.g_avgvis for r in recs], np.float64),
+               lohi=np.array([[r.lo[0], r.lo[1], r.hi[0], r.hi[1]] for r in recs], np.float32).reshape(B, 4))
+    out["objective"] = objective if objective is not None else int(out["g_vis"].max()) if B else 0
+    return out
+
+
+def bo_run(m, n, objective, L=100, seed=0, n_sobol=8):
+    """Host BO driver (no GPU needed) with a Python objective(v, h) -> int."""
+    D = (m - 1) + (n - 1)
+    errs = []
+
+    def cb(ctx, vp, hp, outp):
+        try:
+            v = np.array([vp[i] for i in range(m - 1)], np.float32)
+            h = np.array([hp[i] for i in range(n - 1)], np.float32)
+            outp[0] = int(objective(v, h))
+            return 0
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            return 1
+
+    fn = OBJECTIVE_FN(cb)
+    o = BalanceOpts(int(L), int(seed), 0.1, 0.15, int(n_sobol))
+    v = np.empty(max(m - 1, 1), np.float32)
+    h = np.empty(max(n - 1, 1), np.float32)
+    hist = np.empty(L, np.uint32)
+    ch = np.empty((L, max(D, 1)), np.float32)
+    code = lib().lobe_bo_run(m, n, ctypes.byref(o), fn, None, _ptr(v), _ptr(h), _ptr(hist), _ptr(ch))
+    if errs:
+        raise errs[0]
+    _check(code)
+    return dict(v=v[:m - 1], h=h[:n - 1], history=hist, cut_history=ch[:, :D])

@@ -1,0 +1,291 @@
+"""GPU <-> oracle parity through the C ABI (csrc/liblobe.so).
+
+Bar (BASELINE.json north_star): counts, assignments, rows and masks bit-exact;
+depth statistics within 1e-6 relative.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import make_scene, make_config
+from tests.helpers import mini_scene, nadir_camera
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand_cases.json")))
+D_RTOL = 1e-6
+
+
+def _lobe():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_01767_b200 import lobe
+    return lobe
+
+
+def _grid_kw(g):
+    return dict(v=g["v"], h=g["h"], delta_v=float(g["dv"]), delta_h=float(g["dh"]), tau=float(g["tau"]))
+
+
+def _cmp_percam(a, o_vis, o_asg, sel=None):
+    sl = slice(None) if sel is None else sel
+    assert (a["K"][sl] == o_vis["K"]).all()
+    assert (a["zmin"][sl] == o_vis["zmin"]).all() and (a["zmax"][sl] == o_vis["zmax"]).all()
+    np.testing.assert_allclose(a["D"][sl], o_vis["D"], rtol=D_RTOL, atol=0)
+    assert ((a["D"][sl] == 0) == (o_vis["K"] == 0)).all()
+    assert (a["n"][sl] == o_asg["n"]).all()
+    assert (a["n0"][sl] == o_asg["n0"]).all()
+    assert (a["member"][sl] == o_asg["member"]).all()
+    assert (a["home"][sl] == o_asg["home"]).all()
+
+
+def _cmp_loads(L, o):
+    for k in ("n_cams", "g_blk", "g_vis", "incidences"):
+        assert (L[k] == o[k]).all(), k
+    assert (L["area"] == o["area"]).all()
+    assert (L["g_avgvis"] == o["g_avgvis"]).all()
+    assert (L["lohi"] == o["lohi"]).all()
+    assert L["objective"] == o["objective"]
+
+
+def full_parity(sc, grids, mode=0):
+    lobe = _lobe()
+    with lobe.Scene(sc, sc, assign_mode=mode) as S:
+        o0 = oracle.run(sc, grid=grids[0], mode=mode)
+        c0, rho, au, av = o0["frame"]
+        assert (S.frame["center"] == c0).all() and S.frame["radius"] == rho
+        rows = S.export_rows()
+        assert (rows == o0["vis"]["rows"]).all()
+        for g in grids:
+            o = o0 if g is grids[0] else None
+            if o is None:
+                asg = oracle.assign(sc, o0["pre"], o0["vis"], g)
+                bl = oracle.block_loads(sc, o0["pre"], o0["vis"], asg, g, mode=mode)
+                cr, el = oracle.crop(sc, o0["pre"], g, bl["M"])
+            else:
+                asg, bl, cr, el = o["asg"], o["loads"], o["crop"], o["eligible"]
+            a = S.assign_cameras(g["m"], g["n"], **_grid_kw(g))
+            _cmp_percam(a, o0["vis"], asg)
+            L = S.block_loads(g["m"], g["n"], **_grid_kw(g))
+            _cmp_loads(L, bl)
+            c, e = S.crop_masks(g["m"], g["n"], **_grid_kw(g))
+            assert (c == cr).all() and (e == el).all()
+
+
+def _rand_grid(m, n, seed, **kw):
+    rng = np.random.default_rng(seed)
+    v = np.sort(rng.uniform(0.05, 0.95, m - 1)).astype(np.float32)
+    h = np.sort(rng.uniform(0.05, 0.95, n - 1)).astype(np.float32)
+    return oracle.default_grid(m, n, v=v, h=h, **kw)
+
+
+def test_tiny_full(tiny_scene):
+    full_parity(tiny_scene, [oracle.default_grid(2, 2), oracle.default_grid(1, 1), _rand_grid(3, 3, 1),
+                             oracle.default_grid(2, 2, tau=0.0), oracle.default_grid(2, 2, delta_v=0, delta_h=0)])
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_tiny_modes(tiny_scene, mode):
+    full_parity(tiny_scene, [oracle.default_grid(2, 2), _rand_grid(4, 3, 2)], mode=mode)
+
+
+def test_ragged_multi_tile():
+    """G not a multiple of the tile / chunk / word sizes, N not a multiple of the camera group."""
+    sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x5151))
+    full_parity(sc, [oracle.default_grid(4, 4), _rand_grid(6, 6, 3), _rand_grid(8, 8, 4, tau=0.05),
+                     oracle.default_grid(1, 7), oracle.default_grid(2, 2, tau=1.0)])
+
+
+def test_mid_size():
+    sc = make_scene(make_config("matrixcity", G=150_000, N=120, seed=0x77))
+    full_parity(sc, [oracle.default_grid(6, 6), _rand_grid(5, 4, 9)])
+
+
+@pytest.mark.parametrize("case", GOLD["visibility"], ids=[c["id"] for c in GOLD["visibility"]])
+def test_hand_visibility_gpu(case):
+    lobe = _lobe()
+    anchors = [dict(mu=[-50, -50, -50], s=0.01, o=0.0), dict(mu=[50, 50, 50], s=0.01, o=0.0)]
+    sc = mini_scene([dict(mu=case["mu"], s=case["s"], o=case["o"])] + anchors, [GOLD["camera_C0"]])
+    fr = dict(center=[0, 0, 0], radius=1.0, axis_u=[1, 0, 0], axis_v=[0, 1, 0])
+    with lobe.Scene(sc, sc, frame=fr) as S:
+        rows = S.export_rows()
+        assert bool(rows[0, 0] & 1) == case["visible"], case["id"]
+
+
+def test_hand_depth_H7_gpu():
+    lobe = _lobe()
+    d = GOLD["depth_stat"]
+    g = [dict(mu=x["mu"], s=x["s"], o=x["o"]) for x in d["gaussians"]]
+    g += [dict(mu=[-50, -50, -50], s=0.01, o=0.0), dict(mu=[50, 50, 50], s=0.01, o=0.0)]
+    sc = mini_scene(g, [GOLD["camera_C0"]])
+    with lobe.Scene(sc, sc, frame=dict(center=[0, 0, 0], radius=1.0, axis_u=[1, 0, 0], axis_v=[0, 1, 0])) as S:
+        a = S.assign_cameras(1, 1)
+        assert a["K"][0] == d["K"] and a["D"][0] == pytest.approx(d["D"], rel=1e-15)
+        assert a["zmin"][0] == d["z_min"] and a["zmax"][0] == d["z_max"]
+
+
+def test_hand_assignment_H9_gpu():
+    lobe = _lobe()
+    a = GOLD["assignment"]
+    rng = np.random.default_rng(0)
+    g = [dict(mu=x["mu"], s=x["s"], o=x["o"]) for x in a["anchors"]]
+    for cl in (a["cluster_low"], a["cluster_high"]):
+        for _ in range(cl["count"]):
+            g.append(dict(mu=np.asarray(cl["center"], float) + np.r_[rng.uniform(-0.05, 0.05, 2), 0.0], s=0.001,
+                          o=0.9))
+    sc = mini_scene(g, [nadir_camera(*a["camera"]["nadir_at"], f=a["camera"]["f"])], m=2, n=2)
+    with lobe.Scene(sc, sc, frame=dict(center=[0, 0, 0], radius=10.0, axis_u=[1, 0, 0], axis_v=[0, 1, 0])) as S:
+        r = S.assign_cameras(2, 2, delta_v=0.05, delta_h=0.05, tau=0.15)
+        e = a["expect"]
+        assert r["K"][0] == e["K"] and list(r["n"][0]) == e["n"] and list(r["n0"][0]) == e["n0"]
+        assert [b for b in range(4) if (int(r["member"][0]) >> b) & 1] == e["member_tau_0.15"]
+        assert r["home"][0] == e["home"]
+        r = S.assign_cameras(2, 2, delta_v=0.05, delta_h=0.05, tau=0.5)
+        assert [b for b in range(4) if (int(r["member"][0]) >> b) & 1] == e["member_tau_0.5"]
+
+
+def test_determinism_and_permutation(tiny_scene):
+    lobe = _lobe()
+    sc = tiny_scene
+    with lobe.Scene(sc, sc) as A, lobe.Scene(sc, sc) as B:
+        assert (A.export_rows() == B.export_rows()).all()
+        a, b = A.assign_cameras(2, 2), B.assign_cameras(2, 2)
+        for k in a:
+            assert (a[k] == b[k]).all(), k                      # I11: identical bytes (D included)
+    perm = np.random.default_rng(3).permutation(sc.G)
+    sc2 = sc.permute_gaussians(perm)
+    with lobe.Scene(sc, sc) as A, lobe.Scene(sc2, sc2) as B:
+        la, lb = A.block_loads(2, 2), B.block_loads(2, 2)
+        for k in ("g_vis", "g_blk", "n_cams", "incidences"):
+            assert (la[k] == lb[k]).all()                       # I13
+        ra, rb = A.export_rows(), B.export_rows()
+        ua = np.unpackbits(ra.view(np.uint8), axis=1, bitorder="little")[:, :sc.G]
+        ub = np.unpackbits(rb.view(np.uint8), axis=1, bitorder="little")[:, :sc.G]
+        assert (ub == ua[:, perm]).all()
+
+
+def test_world_shards_match_world1():
+    """Camera sharding on one GPU, ranks run one after another:
+    per-camera outputs concatenate, OR-combined partial masks equal world=1."""
+    import torch
+    lobe = _lobe()
+    sc = make_scene(make_config("rubble", G=60_000, N=41, seed=0x99))
+    m, n = 3, 3
+    with lobe.Scene(sc, sc) as S1:
+        ref = S1.assign_cameras(m, n)
+        L1 = S1.block_loads(m, n)
+        c1, e1 = S1.crop_masks(m, n)
+        words = S1.mask_words()
+    for W in (2, 3):
+        parts, outs, ncs, incs = [], [], [], []
+        scenes = [lobe.Scene(sc, sc, rank=r, world=W) for r in range(W)]
+        try:
+            for S in scenes:
+                outs.append(S.assign_cameras(m, n))
+                d = torch.zeros(m * n * words, dtype=torch.int32, device="cuda")
+                nc, inc = S.block_partial(m, n, d)
+                parts.append(d)
+                ncs.append(nc)
+                incs.append(inc)
+            for k in ref:
+                assert (np.concatenate([o[k] for o in outs]) == ref[k]).all(), k
+            gathered = torch.cat(parts)
+            comb = torch.empty_like(parts[0])
+            gv = scenes[0].masks_combine(m * n, gathered, W, comb)
+            rec = scenes[0].block_records(m, n, np.sum(ncs, axis=0), np.sum(incs, axis=0), gv)
+            for k in ("n_cams", "g_vis", "g_blk", "incidences", "g_avgvis", "area"):
+                assert (rec[k] == L1[k]).all(), k
+            c, e = scenes[W - 1].crop_from_masks(m, n, comb)
+            assert (c == c1).all() and (e == e1).all()
+        finally:
+            for S in scenes:
+                S.close()
+
+
+def test_bo_trajectory_parity_and_I16():
+    """Every evaluation of lobe_balance_partition equals the oracle objective at
+    the recorded cuts (so the oracle-backed run follows the same trajectory), and
+    the visibility kernel ran exactly once: tests_executed = G N (I16)."""
+    lobe = _lobe()
+    sc = make_scene(make_config("building", G=40_000, N=48, seed=0x42))
+    m, n = sc.cfg.m, sc.cfg.n
+    o = oracle.run(sc, grid=oracle.default_grid(m, n), masks=False)
+    with lobe.Scene(sc, sc) as S:
+        r = S.balance_partition(m, n, L=16, seed=5)
+        for row, val in zip(r["cut_history"], r["history"]):
+            g = oracle.default_grid(m, n, v=row[:m - 1], h=row[m - 1:])
+            assert oracle.evaluate_cuts(sc, o["pre"], o["vis"], g) == val
+        assert r["best"]["objective"] == r["history"].min() <= r["history"][0]
+        st = S.stats()
+        assert st.tests_executed == sc.G * sc.N and st.vis_launches == 1
+
+
+@pytest.mark.parametrize("name", ["rubble", "matrixcity"])
+def test_full_size_sampled(name):
+    """BASELINE configs at full size, in the launch configuration bench.py times:
+    rows / per-camera outputs bit-exact on sampled cameras (the oracle computes
+    them one by one), block-level invariants at full size."""
+    lobe = _lobe()
+    sc = make_scene(name)
+    m, n = sc.cfg.m, sc.cfg.n
+    rng = np.random.default_rng(11)
+    sel = np.sort(rng.choice(sc.N, 6, replace=False))
+    with lobe.Scene(sc, sc) as S:
+        fr = oracle.frame(sc)
+        assert (S.frame["center"] == fr[0]).all() and S.frame["radius"] == fr[1]
+        pre = oracle.prep(sc, fr)
+        pre["cam_gu_sel"], pre["cam_gv_sel"] = pre["cam_gu"][sel], pre["cam_gv"][sel]
+        vis = oracle.visibility(sc, pre, cams=sel)
+        rows = np.concatenate([S.export_rows(int(c), 1) for c in sel])
+        assert (rows == vis["rows"]).all()
+        g = oracle.default_grid(m, n)
+        asg = oracle.assign(sc, pre, vis, g)
+        a = S.assign_cameras(m, n)
+        _cmp_percam(a, vis, asg, sel=sel)
+        L = S.block_loads(m, n)
+        assert int(L["incidences"].sum()) == int(a["K"].astype(np.int64).sum())      # I2
+        assert int(L["g_blk"].astype(np.int64).sum()) == sc.G                         # I4
+        assert (a["n0"].sum(axis=1) == a["K"]).all() and (a["n"] >= a["n0"]).all()  # I5, I6
+        for b in range(m * n):
+            cams = np.nonzero((a["member"] >> np.uint64(b)) & np.uint64(1))[0]
+            if len(cams):
+                assert a["K"][cams].max() <= L["g_vis"][b] <= min(sc.G, int(a["K"][cams].astype(np.int64).sum()))
+        # crop superset (I1) for the sampled cameras
+        c, _ = S.crop_masks(m, n, eligible=False)
+        for j, cam in enumerate(sel):
+            rb = np.unpackbits(rows[j].view(np.uint8), bitorder="little")[:sc.G].astype(bool)
+            for b in range(m * n):
+                if (int(a["member"][cam]) >> b) & 1:
+                    cb = np.unpackbits(c[b].view(np.uint8), bitorder="little")[:sc.G].astype(bool)
+                    assert not (rb & ~cb).any()
+
+
+def test_errors_gpu():
+    lobe = _lobe()
+    g = [dict(mu=[0, 0, 5], s=0.1, o=1.0), dict(mu=[1, 1, 5], s=0.1, o=1.0)]
+    sc = mini_scene(g, [GOLD["camera_C0"]])
+    sc.x[0] = np.nan
+    fr = dict(center=[0, 0, 0], radius=1.0, axis_u=[1, 0, 0], axis_v=[0, 1, 0])
+    with pytest.raises(lobe.LobeError) as e:
+        lobe.Scene(sc, sc, frame=fr)
+    assert e.value.status == "INVALID_INPUT"
+    with pytest.raises(lobe.LobeError) as e:      # one camera: automatic radius is 0
+        lobe.Scene(mini_scene(g, [GOLD["camera_C0"]]), mini_scene(g, [GOLD["camera_C0"]]))
+    assert e.value.status == "DEGENERATE_SCENE"
+    sc = mini_scene([dict(mu=[1, 1, 1], s=0.1, o=1.0)] * 3, [GOLD["camera_C0"]])
+    with pytest.raises(lobe.LobeError) as e:
+        lobe.Scene(sc, sc, frame=dict(center=[0, 0, 0], radius=1.0, axis_u=[1, 0, 0], axis_v=[0, 1, 0]))
+    assert e.value.status == "DEGENERATE_SCENE"
+    sc = make_scene(make_config("tiny", G=500, N=4))
+    with lobe.Scene(sc, sc) as S:
+        with pytest.raises(lobe.LobeError) as e:
+            S.block_loads(3, 1, v=np.array([0.6, 0.4], np.float32))
+        assert e.value.status == "INVALID_CUTS"
+        with pytest.raises(lobe.LobeError) as e:
+            S.block_loads(9, 9)
+        assert e.value.status == "INVALID_CONFIG"
+        S.block_loads(2, 2)   # handle still valid after failures
