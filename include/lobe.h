@@ -159,6 +159,8 @@ typedef struct {
   uint64_t vis_launches, evaluations;
   int64_t n_gaussians, n_cameras, n_local_cameras, cam_begin;
   uint64_t tile_pairs; /* (tile, camera) pairs with any visible Gaussian */
+  uint64_t kernel_launches; /* cumulative launches of this library's own kernels */
+  uint64_t cub_launches;    /* cumulative CUB primitive calls (radix sort, scan) */
 } lobe_stats;
 
 /* ---- scene --------------------------------------------------------------- */

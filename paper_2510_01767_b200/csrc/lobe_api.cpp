@@ -49,6 +49,18 @@ lobe_status fail(lobe_status st, const std::string& msg) {
     }                                                                                              \
   } while (0)
 
+// launch of one of this library's kernels (counted for lobe_stats.kernel_launches)
+#define KL(call)                      \
+  do {                                \
+    CK(call);                         \
+    s->st.kernel_launches += 1;       \
+  } while (0)
+#define CUBL(call)                    \
+  do {                                \
+    CK(call);                         \
+    s->st.cub_launches += 1;          \
+  } while (0)
+
 #define TRY(expr)                       \
   do {                                  \
     lobe_status s_ = (expr);            \
@@ -351,13 +363,13 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks, st));
   CK(cudaMemsetAsync(s->incid, 0, sizeof(unsigned long long) * kMaxBlocks, st));
   CK(cudaEventRecord(s->ev[2], st));
-  CK(launch_zones(s->dz, nzv, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
-  CK(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
+  KL(launch_zones(s->dz, nzv, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
+  KL(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
   // ---- a6 histograms
   TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
   if (s->N_loc > 0) {
     CK(cudaMemsetAsync(s->hist, 0, sizeof(uint32_t) * (size_t)s->N_loc * nzp, st));
-    CK(launch_hist(s->n_pairs, s->pair_cam, s->pair_tile, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
+    KL(launch_hist(s->n_pairs, s->pair_cam, s->pair_tile, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
                    s->hist, st));
   }
   CK(cudaEventRecord(s->ev[3], st));
@@ -380,11 +392,11 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
     a.sel = s->sel;
     a.ncams = s->counts;
     a.incid = s->incid;
-    CK(launch_assign(a, st));
+    KL(launch_assign(a, st));
   }
   // ---- a8 block masks
   if (masks_out) {
-    CK(launch_block_masks(s->n_tiles, s->tile_off, s->pair_cam, s->sel, s->rows, s->words, g.B, masks_out,
+    KL(launch_block_masks(s->n_tiles, s->tile_off, s->pair_cam, s->sel, s->rows, s->words, g.B, masks_out,
                           s->counts + kMaxBlocks, st));
   }
   CK(cudaEventRecord(s->ev[4], st));
@@ -587,7 +599,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       pin.av[a] = F.axis_v[a];
     }
     pin.rho = F.radius;
-    CK(launch_prep_raw(pin, ru, rv, kk, scratch, err_idx, scratch + 1, st));
+    KL(launch_prep_raw(pin, ru, rv, kk, scratch, err_idx, scratch + 1, st));
     uint32_t hs[8];
     unsigned long long hbad;
     CK(cudaMemcpyAsync(hs, scratch, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -607,19 +619,19 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
     if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
       return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
-    CK(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, keys, vals, st));
+    KL(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, keys, vals, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st));
     void* tmp = nullptr;
     CK(cudaMallocAsync(&tmp, tmpb, st));
-    CK(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st));
+    CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st));
     CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->o2, (size_t)s->G_pad));
     CK(s->alloc(&s->gu, (size_t)s->G_pad));
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
     CK(s->alloc(&s->iperm, (size_t)G));
-    CK(launch_pack(G, s->G_pad, perm, din[0], din[1], din[2], kk, din[10], gu_c, gv_c, s->xy, s->zk, s->o2, s->gu,
+    KL(launch_pack(G, s->G_pad, perm, din[0], din[1], din[2], kk, din[10], gu_c, gv_c, s->xy, s->zk, s->o2, s->gu,
                    s->gv, s->iperm, st));
     cudaFreeAsync(tmp, st);
     s->release(ru); s->release(rv); s->release(kk); s->release(gu_c); s->release(gv_c);
@@ -671,20 +683,20 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.flags = s->flags;
       va.part = s->part;
       int grid = 0;
-      CK(launch_visibility(va, s->num_sms, st, &grid));
+      KL(launch_visibility(va, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[2], st));
-    if (s->N_loc > 0) CK(launch_reduce_partials(s->part, s->n_chunks, s->N_loc, s->K, s->D, s->zmin, s->zmax, st));
+    if (s->N_loc > 0) KL(launch_reduce_partials(s->part, s->n_chunks, s->N_loc, s->K, s->D, s->zmin, s->zmax, st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
     uint32_t* cnt;
     CK(s->alloc(&cnt, (size_t)s->n_tiles + 1));
     CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
-    if (s->N_loc > 0) CK(launch_tile_count(s->flags, s->n_tiles, s->N_loc, cnt, st));
+    if (s->N_loc > 0) KL(launch_tile_count(s->flags, s->n_tiles, s->N_loc, cnt, st));
     size_t sb = 0;
     CK(exclusive_scan_u32(nullptr, sb, cnt, s->tile_off, s->n_tiles + 1, st));
     CK(cudaMallocAsync(&tmp, sb, st));
-    CK(exclusive_scan_u32(tmp, sb, cnt, s->tile_off, s->n_tiles + 1, st));
+    CUBL(exclusive_scan_u32(tmp, sb, cnt, s->tile_off, s->n_tiles + 1, st));
     cudaFreeAsync(tmp, st);
     s->release(cnt);
     uint32_t np = 0;
@@ -694,7 +706,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->pair_cam, (size_t)np));
     CK(s->alloc(&s->pair_tile, (size_t)np));
     if (s->N_loc > 0 && np > 0)
-      CK(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
+      KL(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
     CK(s->alloc(&s->word_zone, (size_t)s->words));
@@ -805,7 +817,7 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   if (crop) CK(s->alloc(&dc, bytes / 4));
   if (eligible) CK(s->alloc(&de, bytes / 4));
   CK(cudaEventRecord(s->ev[5], s->stream));
-  CK(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, dc, de, s->stream));
+  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, dc, de, s->stream));
   CK(cudaEventRecord(s->ev[6], s->stream));
   TRY(copy_out(s, crop, dc, bytes));
   TRY(copy_out(s, eligible, de, bytes));
@@ -840,7 +852,7 @@ lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathe
   CK(cudaSetDevice(s->device));
   CK(cudaMemsetAsync(s->counts + kMaxBlocks, 0, sizeof(uint32_t) * kMaxBlocks, s->stream));
   CK(cudaEventRecord(s->ev[5], s->stream));
-  CK(launch_masks_combine(d_gathered, W, B, s->words, d_out, s->counts + kMaxBlocks, s->stream));
+  KL(launch_masks_combine(d_gathered, W, B, s->words, d_out, s->counts + kMaxBlocks, s->stream));
   CK(cudaEventRecord(s->ev[6], s->stream));
   if (g_vis) CK(cudaMemcpyAsync(g_vis, s->counts + kMaxBlocks, sizeof(uint32_t) * B, cudaMemcpyDefault, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -868,7 +880,7 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
   const size_t W32 = (size_t)((s->G + 31) / 32);
   uint32_t* d = nullptr;
   CK(s->alloc(&d, W32 * count));
-  CK(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, d, s->stream));
+  KL(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, d, s->stream));
   TRY(copy_out(s, rows, d, W32 * count * 4));
   s->release(d);
   CK(cudaStreamSynchronize(s->stream));

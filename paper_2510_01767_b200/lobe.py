@@ -79,7 +79,8 @@ class Stats(ctypes.Structure):
                [(k, ctypes.c_uint64) for k in ("tests_executed", "bytes_read", "bytes_written", "vis_launches",
                                                "evaluations")] + \
                [(k, ctypes.c_int64) for k in ("n_gaussians", "n_cameras", "n_local_cameras", "cam_begin")] + \
-               [("tile_pairs", ctypes.c_uint64)]
+               [("tile_pairs", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("cub_launches", ctypes.c_uint64)]
 
 
 OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
@@ -184,7 +185,9 @@ class Scene:
         self._keep = []
         names = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
         arrs = [getattr(gaussians, k) for k in names]
-        on_dev = int(not isinstance(arrs[0], np.ndarray))
+        on_dev = int(getattr(arrs[0], "is_cuda", False))
+        if not on_dev and not isinstance(arrs[0], np.ndarray):
+            arrs = [a.numpy() for a in arrs]     # host torch tensors (e.g. pinned) -> numpy views
         if not on_dev:
             arrs = [np.ascontiguousarray(a, np.float32) for a in arrs]
         self._keep.append(arrs)
@@ -269,7 +272,7 @@ class Scene:
 
     def crop_masks_into(self, m, n, crop_ptr, elig_ptr, **grid_kw):
         g, keep = make_grid(m, n, **grid_kw)
-        _check(lib().lobe_crop_masks(self.handle, ctypes.byref(g), crop_ptr, elig_ptr))
+        _check(lib().lobe_crop_masks(self.handle, ctypes.byref(g), _ptr(crop_ptr), _ptr(elig_ptr)))
 
     def balance_partition(self, m, n, L=100, seed=0, delta_scale=0.1, tau=0.15, n_sobol=8):
         o = BalanceOpts(int(L), int(seed), float(delta_scale), float(tau), int(n_sobol))
@@ -315,6 +318,11 @@ class Scene:
         _check(lib().lobe_block_records(self.handle, ctypes.byref(g), _ptr(n_cams), _ptr(incid), _ptr(g_vis), recs,
                                         ctypes.byref(obj)))
         return records_to_dict(recs, int(obj.value))
+
+    def crop_from_masks_into(self, m, n, d_masks, crop_ptr, elig_ptr, **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        _check(lib().lobe_crop_from_masks(self.handle, ctypes.byref(g), _ptr(d_masks), _ptr(crop_ptr),
+                                          _ptr(elig_ptr)))
 
     def crop_from_masks(self, m, n, d_masks, crop=True, eligible=True, **grid_kw):
         g, keep = make_grid(m, n, **grid_kw)
