@@ -243,6 +243,11 @@ lobe_status lobe_crop_from_masks(lobe_scene* scene, const lobe_grid* grid, const
  * count x ceil(G/32) u32, bit (i mod 32) of word i/32 (for parity tests). */
 lobe_status lobe_export_rows(lobe_scene* scene, int64_t c0, int64_t count, uint32_t* rows);
 lobe_status lobe_get_stats(const lobe_scene* scene, lobe_stats* out);
+/* Tuning: re-run the visibility kernel (a3) of this scene with kernel variant
+ * `variant` (0 = default; all variants produce identical bytes) `reps` times on
+ * options.stream; *ms = mean CUDA-event time per launch, *grid = CTAs launched.
+ * LOBE_E_INVALID_INDEX for an unknown variant. */
+lobe_status lobe_dev_vis_bench(lobe_scene* scene, int32_t variant, int32_t reps, float* ms, int32_t* grid);
 /* Library build info string (arch, flags). */
 const char* lobe_version(void);
 

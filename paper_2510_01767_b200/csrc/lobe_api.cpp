@@ -887,6 +887,34 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
   return LOBE_OK;
 }
 
+lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (variant < 0 || variant >= num_visibility_variants()) return fail(LOBE_E_INVALID_INDEX, "variant");
+  if (s->N_loc <= 0 || reps < 1) return fail(LOBE_E_INVALID_CONFIG, "nothing to run");
+  CK(cudaSetDevice(s->device));
+  VisArgs va{};
+  va.xy = reinterpret_cast<const float4*>(s->xy);
+  va.zk = reinterpret_cast<const float4*>(s->zk);
+  va.o2 = reinterpret_cast<const float2*>(s->o2);
+  va.cams = s->cams;
+  va.n_cams = s->N_loc;
+  va.n_chunks = s->n_chunks;
+  va.words = s->words;
+  va.rows = s->rows;
+  va.flags = s->flags;
+  va.part = s->part;
+  int g = 0;
+  KL(launch_visibility_variant(variant, va, s->num_sms, s->stream, &g));  // warm
+  CK(cudaEventRecord(s->ev[6], s->stream));
+  for (int r = 0; r < reps; ++r) KL(launch_visibility_variant(variant, va, s->num_sms, s->stream, &g));
+  CK(cudaEventRecord(s->ev[7], s->stream));
+  CK(cudaEventSynchronize(s->ev[7]));
+  if (ms) *ms = ms_between(s->ev[6], s->ev[7]) / reps;
+  if (grid) *grid = g;
+  return LOBE_OK;
+}
+
 lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
   *out = s->st;

@@ -81,6 +81,9 @@ struct VisArgs {
   VisPartial* part;    // [n_chunks x n_cams]
 };
 cudaError_t launch_visibility(const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
+// tuning variants of the same kernel (bit-identical outputs)
+int num_visibility_variants();
+cudaError_t launch_visibility_variant(int variant, const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
 // a4: reduce partials in chunk order -> K, D, zmin, zmax.
 cudaError_t launch_reduce_partials(const VisPartial* part, int64_t n_chunks, int64_t n_cams, uint32_t* K, double* D,
                                    float* zmin, float* zmax, cudaStream_t st);

@@ -23,7 +23,7 @@ FRAME_AUTO_CENTER, FRAME_AUTO_RADIUS, FRAME_AUTO_AXES, FRAME_AUTO_ALL = 1, 2, 4,
 EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign_cameras", "lobe_block_loads",
            "lobe_crop_masks", "lobe_balance_partition", "lobe_bo_run", "lobe_mask_words", "lobe_block_partial",
            "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
-           "lobe_get_stats", "lobe_version"]
+           "lobe_get_stats", "lobe_version", "lobe_dev_vis_bench"]
 
 
 class LobeError(RuntimeError):
@@ -117,6 +117,7 @@ def lib():
         L.lobe_crop_from_masks.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
         L.lobe_export_rows.argtypes = [vp, i64, i64, vp]
         L.lobe_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+        L.lobe_dev_vis_bench.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
         for name in EXPORTS:
             if name not in ("lobe_last_error", "lobe_version", "lobe_mask_words", "lobe_free_scene"):
                 getattr(L, name).restype = ctypes.c_int
@@ -291,6 +292,12 @@ class Scene:
         out = np.empty((count, (self.G + 31) // 32), np.uint32)
         _check(lib().lobe_export_rows(self.handle, int(c0), int(count), _ptr(out)))
         return out
+
+    def dev_vis_bench(self, variant=0, reps=3):
+        ms = ctypes.c_float()
+        grid = ctypes.c_int32()
+        _check(lib().lobe_dev_vis_bench(self.handle, int(variant), int(reps), ctypes.byref(ms), ctypes.byref(grid)))
+        return float(ms.value), int(grid.value)
 
     def mask_words(self):
         return int(lib().lobe_mask_words(self.handle))
