@@ -262,6 +262,7 @@ def main():
     with ClockSampler(torch.cuda.current_device()) as clk:
         ms, (Lrec, Aout) = timed(args.steps, dg, crop_d, elig_d)
     t_vis = statistics.mean(stats_acc["t_vis_ms"])
+    timed_kernels, timed_cub = stats_acc["kernels"], stats_acc["cub"]
     n_local = N // world if world > 1 else N
     value = G * N / (ms * 1e-3)
 
@@ -345,10 +346,10 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": G * N / (ms_e2e * 1e-3), "unit": "tests/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
-            "gpu_launches": int(stats_acc["kernels"]),
+            "gpu_launches": int(timed_kernels),
             "gpu_launches_note": f"own kernels in the timed region ({args.steps} steps, rank 0), "
-                                 f"{stats_acc['kernels'] / args.steps:.0f} per step; plus CUB primitive calls "
-                                 f"(radix sort, scan): {stats_acc['cub'] / args.steps:.0f} per step",
+                                 f"{timed_kernels / args.steps:.0f} per step; plus CUB primitive calls "
+                                 f"(radix sort, scan): {timed_cub / args.steps:.0f} per step",
             "clocks": clocks, "bo": bo,
             "objective_uniform": int(Lrec["objective"]),
             "visible_incidences": int(np.asarray(Aout["K"], np.int64).sum()),
