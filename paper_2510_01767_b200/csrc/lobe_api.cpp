@@ -98,7 +98,14 @@ struct lobe_scene {
   float *d_cam_gu = nullptr, *d_cam_gv = nullptr;
   uint32_t* rows = nullptr;
   uint8_t* flags = nullptr;
-  VisPartial* part = nullptr;
+  PairPartial* pair_part = nullptr;
+  uint32_t* cam_off = nullptr;
+  int32_t* cam_order = nullptr;
+  float4 *tile_lo = nullptr, *tile_hi = nullptr;
+  CullRow* cull = nullptr;
+  uint32_t* keep = nullptr;
+  unsigned long long* kept = nullptr;
+  int64_t n_sub = 0;
   uint32_t* K = nullptr;
   double* D = nullptr;
   float *zmin = nullptr, *zmax = nullptr;
@@ -234,6 +241,23 @@ CamSetup camera_setup(const lobe_camera& k) {
   s.zn = k.z_near;
   s.zf = k.z_far;
   return s;
+}
+
+// Tile-culling forms (fp64 of the fp32 setup): w, u, v, eu = u - Wf w, ev = v - Hf w.
+CullRow cull_row(const CamSetup& c) {
+  CullRow r{};
+  for (int i = 0; i < 4; ++i) {
+    r.f[0][i] = c.Aw[i];
+    r.f[1][i] = c.Au[i];
+    r.f[2][i] = c.Av[i];
+    r.f[3][i] = (double)c.Au[i] - (double)c.Wf * (double)c.Aw[i];
+    r.f[4][i] = (double)c.Av[i] - (double)c.Hf * (double)c.Aw[i];
+  }
+  r.zn = c.zn;
+  r.zf = c.zf;
+  r.Wf = c.Wf;
+  r.Hf = c.Hf;
+  return r;
 }
 
 // O3's fp32 map for one point (contraction + ground projection), host side.
@@ -497,7 +521,8 @@ void lobe_free_scene(lobe_scene* s) {
   cudaSetDevice(s->device);
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
-  s->release(s->rows); s->release(s->flags); s->release(s->part); s->release(s->K); s->release(s->D);
+  s->release(s->rows); s->release(s->flags); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
@@ -599,7 +624,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       pin.av[a] = F.axis_v[a];
     }
     pin.rho = F.radius;
-    KL(launch_prep_raw(pin, ru, rv, kk, scratch, err_idx, scratch + 1, st));
+    KL(launch_prep_raw(pin, ru, rv, kk, keys, vals, scratch, err_idx, scratch + 1, st));
     uint32_t hs[8];
     unsigned long long hbad;
     CK(cudaMemcpyAsync(hs, scratch, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -619,7 +644,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
     if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
       return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
-    KL(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, keys, vals, st));
+    KL(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st));
     void* tmp = nullptr;
@@ -641,11 +666,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
 
     // ---- a2 camera setup (local shard) + camera-centre grid coords
     std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
+    std::vector<CullRow> hcull(std::max<int64_t>(s->N_loc, 1));
     s->cam_gu.assign(s->N_loc, 0.f);
     s->cam_gv.assign(s->N_loc, 0.f);
     for (int64_t c = 0; c < s->N_loc; ++c) {
       const lobe_camera& k = cams[s->cam_begin + c];
       hset[c] = camera_setup(k);
+      hcull[c] = cull_row(hset[c]);
       double oc[3];
       cam_centre(k, oc);
       float ru_, rv_;
@@ -660,6 +687,15 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->d_cam_gu, NL));
     CK(s->alloc(&s->d_cam_gv, NL));
     CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, st));
+    s->n_sub = (NL + 31) / 32;
+    CK(s->alloc(&s->cull, NL));
+    CK(cudaMemcpyAsync(s->cull, hcull.data(), sizeof(CullRow) * NL, cudaMemcpyHostToDevice, st));
+    CK(s->alloc(&s->tile_lo, (size_t)s->n_tiles));
+    CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
+    CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
+    CK(s->alloc(&s->kept, 1));
+    KL(launch_tile_bounds(reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk), s->n_tiles,
+                          s->tile_lo, s->tile_hi, st));
     if (s->N_loc > 0) {
       CK(cudaMemcpyAsync(s->d_cam_gu, s->cam_gu.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(s->d_cam_gv, s->cam_gv.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
@@ -667,9 +703,12 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // ---- a3/a4 visibility pass
     CK(s->alloc(&s->rows, (size_t)NL * s->words));
     CK(s->alloc(&s->flags, (size_t)s->n_tiles * NL));
-    CK(s->alloc(&s->part, (size_t)s->n_chunks * NL));
+    CK(cudaMemsetAsync(s->flags, 0, (size_t)s->n_tiles * NL, st));
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
+    CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
+    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
+    CK(cudaEventRecord(s->ev[7], st));
     if (s->N_loc > 0) {
       VisArgs va{};
       va.xy = reinterpret_cast<const float4*>(s->xy);
@@ -681,12 +720,12 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.words = s->words;
       va.rows = s->rows;
       va.flags = s->flags;
-      va.part = s->part;
+      va.keep = s->keep;
+      va.n_sub = s->n_sub;
       int grid = 0;
       KL(launch_visibility(va, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[2], st));
-    if (s->N_loc > 0) KL(launch_reduce_partials(s->part, s->n_chunks, s->N_loc, s->K, s->D, s->zmin, s->zmax, st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
     uint32_t* cnt;
@@ -707,6 +746,44 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->pair_tile, (size_t)np));
     if (s->N_loc > 0 && np > 0)
       KL(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
+    // ---- a4 depth statistic over the non-empty (tile, camera) pairs
+    CK(cudaEventRecord(s->ev[4], st));
+    CK(s->alloc(&s->pair_part, (size_t)std::max<int64_t>(np, 1)));
+    CK(s->alloc(&s->cam_off, (size_t)NL + 1));
+    CK(s->alloc(&s->cam_order, (size_t)std::max<int64_t>(np, 1)));
+    if (s->N_loc > 0) {
+      KL(launch_depth_pairs(np, s->pair_cam, s->pair_tile, s->rows, s->words, reinterpret_cast<const float4*>(s->xy),
+                            reinterpret_cast<const float4*>(s->zk), reinterpret_cast<const float2*>(s->o2), s->cams,
+                            s->pair_part, st));
+      uint32_t* ccount;
+      CK(s->alloc(&ccount, (size_t)NL + 1));
+      CK(cudaMemsetAsync(ccount, 0, sizeof(uint32_t) * (NL + 1), st));
+      KL(launch_cam_counts(np, s->pair_cam, ccount, st));
+      size_t sb2 = 0;
+      CK(exclusive_scan_u32(nullptr, sb2, ccount, s->cam_off, NL + 1, st));
+      void* tmp2 = nullptr;
+      CK(cudaMallocAsync(&tmp2, sb2, st));
+      CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
+      cudaFreeAsync(tmp2, st);
+      s->release(ccount);
+      if (np > 0) {  // pair indices ordered by camera, tile order kept (stable)
+        uint32_t* ksorted;
+        int32_t* iota;
+        CK(s->alloc(&ksorted, (size_t)np));
+        CK(s->alloc(&iota, (size_t)np));
+        KL(launch_iota(iota, np, st));
+        size_t sb3 = 0;
+        CK(radix_sort_pairs(nullptr, sb3, s->pair_cam, ksorted, iota, s->cam_order, np, st));
+        void* tmp3 = nullptr;
+        CK(cudaMallocAsync(&tmp3, sb3, st));
+        CUBL(radix_sort_pairs(tmp3, sb3, s->pair_cam, ksorted, iota, s->cam_order, np, st));
+        cudaFreeAsync(tmp3, st);
+        s->release(ksorted);
+        s->release(iota);
+      }
+      KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
+    }
+    CK(cudaEventRecord(s->ev[5], st));
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
     CK(s->alloc(&s->word_zone, (size_t)s->words));
@@ -723,6 +800,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaStreamSynchronize(st));
     s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
     s->st.t_vis_ms = ms_between(s->ev[1], s->ev[2]);
+    s->st.t_cull_ms = ms_between(s->ev[1], s->ev[7]);
+    s->st.t_depth_ms = ms_between(s->ev[4], s->ev[5]);
+    {
+      unsigned long long kp = 0;
+      CK(cudaMemcpy(&kp, s->kept, sizeof(kp), cudaMemcpyDeviceToHost));
+      s->st.dense_tests = (uint64_t)kp * (uint64_t)kTile;
+    }
     s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
     s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
     s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
@@ -880,7 +964,7 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
   const size_t W32 = (size_t)((s->G + 31) / 32);
   uint32_t* d = nullptr;
   CK(s->alloc(&d, W32 * count));
-  KL(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, d, s->stream));
+  KL(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, s->flags, s->N_loc, d, s->stream));
   TRY(copy_out(s, rows, d, W32 * count * 4));
   s->release(d);
   CK(cudaStreamSynchronize(s->stream));
@@ -903,7 +987,8 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.words = s->words;
   va.rows = s->rows;
   va.flags = s->flags;
-  va.part = s->part;
+  va.keep = s->keep;
+  va.n_sub = s->n_sub;
   int g = 0;
   KL(launch_visibility_variant(variant, va, s->num_sms, s->stream, &g));  // warm
   CK(cudaEventRecord(s->ev[6], s->stream));

@@ -25,13 +25,13 @@ struct __align__(16) CamSetup {
 };
 static_assert(sizeof(CamSetup) == 64, "CamSetup layout");
 
-// Per (chunk, camera) partial depth statistics written by the visibility kernel.
-struct __align__(16) VisPartial {
-  double S, O;       // sum o*w, sum o over visible Gaussians of the chunk
+// Per non-empty (tile, camera) pair: partial depth statistics (a4).
+struct __align__(16) PairPartial {
+  double S, O;       // sum o*w, sum o over the visible Gaussians of the pair
   float zmin, zmax;  // min/max w
   uint32_t K, pad;
 };
-static_assert(sizeof(VisPartial) == 32, "VisPartial layout");
+static_assert(sizeof(PairPartial) == 32, "PairPartial layout");
 
 // Zone tables for one grid (a5): per axis, sorted breakpoints P[0..nz-2] with
 // P[0] = 0; zone z < nz-1 is [P[z], P[z+1]) (P[nz-1] := 1), zone nz-1 is {1}.
@@ -55,11 +55,12 @@ struct PrepIn {
 };
 // Validation + per-Gaussian raw ground coords and footprint radius. err[0] =
 // error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
-cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* err,
-                            unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
-// Normalise to [0,1], Morton key, identity values.
+// Also writes the 3D Morton sort key of the contracted centre and identity values.
+cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* keys, int32_t* vals,
+                            uint32_t* err, unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
+// Normalise the ground coordinates to [0,1].
 cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, float* gu, float* gv,
-                             uint32_t* keys, int32_t* vals, cudaStream_t st);
+                             cudaStream_t st);
 cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                              int32_t* vout, int64_t n, cudaStream_t st);
 // Gather into the internal pair-interleaved layout, build the inverse permutation.
@@ -77,16 +78,34 @@ struct VisArgs {
   int64_t n_chunks;
   int64_t words;       // row stride in u32 words (G_pad / 32)
   uint32_t* rows;
-  uint8_t* flags;      // [n_tiles x n_cams]
-  VisPartial* part;    // [n_chunks x n_cams]
+  uint8_t* flags;      // [n_tiles x n_cams], zeroed before the pass; 1 = some Gaussian visible
+  const uint32_t* keep;  // [n_tiles x n_sub] camera masks surviving tile culling (NULL: dense)
+  int64_t n_sub;         // ceil(n_cams / 32)
 };
+
+// Tile culling: per camera the five linear forms of the
+// test (w, u, v, eu, ev as c . p + c0, fp64 from the fp32 setup) and the depth
+// range; per tile the AABB of its non-gated Gaussian centres and max k.
+struct CullRow {
+  double f[5][4];  // w, u, v, eu, ev: {c_x, c_y, c_z, c_0}
+  float zn, zf, Wf, Hf;
+};
+cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_tiles, float4* tlo, float4* thi,
+                               cudaStream_t st);
+cudaError_t launch_cull(const float4* tlo, const float4* thi, int64_t n_tiles, const CullRow* rows, int64_t n_cams,
+                        uint32_t* keep, unsigned long long* kept_pairs, cudaStream_t st);
 cudaError_t launch_visibility(const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
 // tuning variants of the same kernel (bit-identical outputs)
 int num_visibility_variants();
 cudaError_t launch_visibility_variant(int variant, const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
-// a4: reduce partials in chunk order -> K, D, zmin, zmax.
-cudaError_t launch_reduce_partials(const VisPartial* part, int64_t n_chunks, int64_t n_cams, uint32_t* K, double* D,
-                                   float* zmin, float* zmax, cudaStream_t st);
+// a4: depth statistic per non-empty (tile, camera) pair, then per camera in tile order.
+cudaError_t launch_depth_pairs(int64_t n_pairs, const uint32_t* pair_cam, const uint32_t* pair_tile,
+                               const uint32_t* rows, int64_t words, const float4* xy, const float4* zk,
+                               const float2* o2, const CamSetup* cams, PairPartial* out, cudaStream_t st);
+cudaError_t launch_cam_counts(int64_t n_pairs, const uint32_t* pair_cam, uint32_t* counts, cudaStream_t st);
+cudaError_t launch_iota(int32_t* v, int64_t n, cudaStream_t st);
+cudaError_t launch_depth_reduce(int64_t n_cams, const uint32_t* cam_off, const int32_t* order, const PairPartial* part,
+                                uint32_t* K, double* D, float* zmin, float* zmax, cudaStream_t st);
 // tile -> camera lists (CSR) from flags.
 cudaError_t launch_tile_count(const uint8_t* flags, int64_t n_tiles, int64_t n_cams, uint32_t* counts,
                               cudaStream_t st);
@@ -134,7 +153,7 @@ cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, con
                         const uint32_t* masks, int64_t words, int B, uint32_t* crop32, uint32_t* elig32,
                         cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
-                               int64_t count, uint32_t* out, cudaStream_t st);
+                               int64_t count, const uint8_t* flags, int64_t n_cams, uint32_t* out, cudaStream_t st);
 // G_blk from per-zone-pair counts.
 cudaError_t launch_gblk(const ZoneTables* dz, int nzv, int nzp, const uint32_t* zp_count, uint32_t* gblk,
                         cudaStream_t st);

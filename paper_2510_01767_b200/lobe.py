@@ -79,7 +79,9 @@ class Stats(ctypes.Structure):
                [(k, ctypes.c_uint64) for k in ("tests_executed", "bytes_read", "bytes_written", "vis_launches",
                                                "evaluations")] + \
                [(k, ctypes.c_int64) for k in ("n_gaussians", "n_cameras", "n_local_cameras", "cam_begin")] + \
-               [("tile_pairs", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+               [("tile_pairs", ctypes.c_uint64), ("dense_tests", ctypes.c_uint64), ("t_cull_ms", ctypes.c_double),
+                ("t_depth_ms", ctypes.c_double),
+                ("kernel_launches", ctypes.c_uint64),
                 ("cub_launches", ctypes.c_uint64)]
 
 
