@@ -105,6 +105,9 @@ struct lobe_scene {
   CullRow* cull = nullptr;
   uint32_t* keep = nullptr;
   unsigned long long* kept = nullptr;
+  uint32_t *koff = nullptr, *klist = nullptr, *unit_tile = nullptr;
+  int64_t n_units = 0;
+  unsigned long long* queue = nullptr;
   int64_t n_sub = 0;
   uint32_t* K = nullptr;
   double* D = nullptr;
@@ -522,7 +525,8 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept); s->release(s->K); s->release(s->D);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept);
+  s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
@@ -708,8 +712,52 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
     if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
+    // kept-camera lists per tile (CSR)
+    unsigned long long kept_pairs = 0;
+    CK(cudaMemcpyAsync(&kept_pairs, s->kept, sizeof(kept_pairs), cudaMemcpyDeviceToHost, st));
+    CK(s->alloc(&s->koff, (size_t)s->n_tiles + 1));
+    {
+      uint32_t* kc;
+      CK(s->alloc(&kc, (size_t)s->n_tiles + 1));
+      CK(cudaMemsetAsync(kc, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
+      if (s->N_loc > 0) KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, kc, nullptr, nullptr, 0, st));
+      size_t sbk = 0;
+      CK(exclusive_scan_u32(nullptr, sbk, kc, s->koff, s->n_tiles + 1, st));
+      void* tk = nullptr;
+      CK(cudaMallocAsync(&tk, sbk, st));
+      CUBL(exclusive_scan_u32(tk, sbk, kc, s->koff, s->n_tiles + 1, st));
+      cudaFreeAsync(tk, st);
+      s->release(kc);
+    }
+    // work units (tile, <= kVisUnit kept cameras)
+    uint32_t *uc, *uoff;
+    CK(s->alloc(&uc, (size_t)s->n_tiles + 1));
+    CK(s->alloc(&uoff, (size_t)s->n_tiles + 1));
+    CK(cudaMemsetAsync(uc, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
+    KL(launch_units(s->koff, s->n_tiles, kVisUnit, uc, nullptr, nullptr, 0, 0, st));
+    {
+      size_t sbu = 0;
+      CK(exclusive_scan_u32(nullptr, sbu, uc, uoff, s->n_tiles + 1, st));
+      void* tu = nullptr;
+      CK(cudaMallocAsync(&tu, sbu, st));
+      CUBL(exclusive_scan_u32(tu, sbu, uc, uoff, s->n_tiles + 1, st));
+      cudaFreeAsync(tu, st);
+    }
+    uint32_t nu = 0;
+    CK(cudaMemcpyAsync(&nu, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    s->n_units = nu;
+    CK(s->alloc(&s->klist, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
+    CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
+    CK(s->alloc(&s->queue, 1));
+    if (s->N_loc > 0 && kept_pairs > 0) {
+      KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, 1, st));
+      KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile, nu, 1, st));
+    }
+    s->release(uc);
+    s->release(uoff);
     CK(cudaEventRecord(s->ev[7], st));
-    if (s->N_loc > 0) {
+    if (s->N_loc > 0 && kept_pairs > 0) {
       VisArgs va{};
       va.xy = reinterpret_cast<const float4*>(s->xy);
       va.zk = reinterpret_cast<const float4*>(s->zk);
@@ -723,7 +771,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.keep = s->keep;
       va.n_sub = s->n_sub;
       int grid = 0;
-      KL(launch_visibility(va, s->num_sms, st, &grid));
+      KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[2], st));
     // ---- (tile, camera) lists
@@ -752,7 +800,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->cam_off, (size_t)NL + 1));
     CK(s->alloc(&s->cam_order, (size_t)std::max<int64_t>(np, 1)));
     if (s->N_loc > 0) {
-      KL(launch_depth_pairs(np, s->pair_cam, s->pair_tile, s->rows, s->words, reinterpret_cast<const float4*>(s->xy),
+      KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, reinterpret_cast<const float4*>(s->xy),
                             reinterpret_cast<const float4*>(s->zk), reinterpret_cast<const float2*>(s->o2), s->cams,
                             s->pair_part, st));
       uint32_t* ccount;
@@ -802,11 +850,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->st.t_vis_ms = ms_between(s->ev[1], s->ev[2]);
     s->st.t_cull_ms = ms_between(s->ev[1], s->ev[7]);
     s->st.t_depth_ms = ms_between(s->ev[4], s->ev[5]);
-    {
-      unsigned long long kp = 0;
-      CK(cudaMemcpy(&kp, s->kept, sizeof(kp), cudaMemcpyDeviceToHost));
-      s->st.dense_tests = (uint64_t)kp * (uint64_t)kTile;
-    }
+    s->st.dense_tests = (uint64_t)kept_pairs * (uint64_t)kTile;
     s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
     s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
     s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
@@ -972,9 +1016,11 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
 }
 
 lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
+  // variant 0: tile-major kernel over the kept lists (production);
+  // 1-5: the camera-inner kernel (1 = culled, 2 = dense: every test evaluated)
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
-  if (variant < 0 || variant >= num_visibility_variants()) return fail(LOBE_E_INVALID_INDEX, "variant");
+  if (variant < 0 || variant >= 1 + num_visibility_variants()) return fail(LOBE_E_INVALID_INDEX, "variant");
   if (s->N_loc <= 0 || reps < 1) return fail(LOBE_E_INVALID_CONFIG, "nothing to run");
   CK(cudaSetDevice(s->device));
   VisArgs va{};
@@ -990,9 +1036,14 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.keep = s->keep;
   va.n_sub = s->n_sub;
   int g = 0;
-  KL(launch_visibility_variant(variant, va, s->num_sms, s->stream, &g));  // warm
+  auto run = [&]() -> cudaError_t {
+    if (variant == 0)
+      return launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, s->stream, &g);
+    return launch_visibility_variant(variant - 1, va, s->num_sms, s->stream, &g);
+  };
+  KL(run());  // warm
   CK(cudaEventRecord(s->ev[6], s->stream));
-  for (int r = 0; r < reps; ++r) KL(launch_visibility_variant(variant, va, s->num_sms, s->stream, &g));
+  for (int r = 0; r < reps; ++r) KL(run());
   CK(cudaEventRecord(s->ev[7], s->stream));
   CK(cudaEventSynchronize(s->ev[7]));
   if (ms) *ms = ms_between(s->ev[6], s->ev[7]) / reps;

@@ -94,12 +94,20 @@ cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_til
                                cudaStream_t st);
 cudaError_t launch_cull(const float4* tlo, const float4* thi, int64_t n_tiles, const CullRow* rows, int64_t n_cams,
                         uint32_t* keep, unsigned long long* kept_pairs, cudaStream_t st);
-cudaError_t launch_visibility(const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
+// kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
+cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
+                              const uint32_t* offs, uint32_t* list, int phase, cudaStream_t st);
+// tile-major visibility over the kept lists: work units = (tile, <= kVisUnit cameras)
+constexpr int kVisUnit = 64;
+cudaError_t launch_units(const uint32_t* koff, int64_t n_tiles, int cmax, uint32_t* uc, const uint32_t* uoff,
+                         uint32_t* unit_tile, int64_t n_units, int phase, cudaStream_t st);
+cudaError_t launch_vis_tiles(const VisArgs& a, const uint32_t* koff, const uint32_t* klist, const uint32_t* unit_tile,
+                             int64_t n_units, unsigned long long* queue, int num_sms, cudaStream_t st, int* grid_out);
 // tuning variants of the same kernel (bit-identical outputs)
 int num_visibility_variants();
 cudaError_t launch_visibility_variant(int variant, const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
 // a4: depth statistic per non-empty (tile, camera) pair, then per camera in tile order.
-cudaError_t launch_depth_pairs(int64_t n_pairs, const uint32_t* pair_cam, const uint32_t* pair_tile,
+cudaError_t launch_depth_pairs(int64_t n_tiles, const uint32_t* tile_off, const uint32_t* pair_cam,
                                const uint32_t* rows, int64_t words, const float4* xy, const float4* zk,
                                const float2* o2, const CamSetup* cams, PairPartial* out, cudaStream_t st);
 cudaError_t launch_cam_counts(int64_t n_pairs, const uint32_t* pair_cam, uint32_t* counts, cudaStream_t st);

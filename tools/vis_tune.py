@@ -31,7 +31,7 @@ def main():
     ref_rows = np.concatenate([S.export_rows(c, 1) for c in sel])
     ref = S.assign_cameras(m, n)
     out = []
-    nv = 5
+    nv = 6
     for v in (variants or range(nv)):
         try:
             ms, grid = S.dev_vis_bench(v, reps)
