@@ -101,7 +101,7 @@ struct lobe_scene {
   PairPartial* pair_part = nullptr;
   uint32_t* cam_off = nullptr;
   int32_t* cam_order = nullptr;
-  float4 *tile_lo = nullptr, *tile_hi = nullptr;
+  float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
   CullRow* cull = nullptr;
   uint32_t* keep = nullptr;
   unsigned long long* kept = nullptr;
@@ -390,7 +390,7 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks, st));
   CK(cudaMemsetAsync(s->incid, 0, sizeof(unsigned long long) * kMaxBlocks, st));
   CK(cudaEventRecord(s->ev[2], st));
-  KL(launch_zones(s->dz, nzv, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
+  KL(launch_zones(s->dz, nzv, nzp, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
   KL(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
   // ---- a6 histograms
   TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
@@ -525,7 +525,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -606,12 +606,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       for (int k = 0; k < 11; ++k) din[k] = src[k];
     }
     // ---- a1 precompute
-    float *ru, *rv, *kk, *gu_c, *gv_c;
+    float *ru, *rv, *kk;
+    float4* rec;
     uint32_t *keys, *keys_s, *scratch;
     int32_t *vals, *perm;
     unsigned long long* err_idx;
     CK(s->alloc(&ru, G)); CK(s->alloc(&rv, G)); CK(s->alloc(&kk, G));
-    CK(s->alloc(&gu_c, G)); CK(s->alloc(&gv_c, G));
+    CK(s->alloc(&rec, (size_t)2 * G));
     CK(s->alloc(&keys, G)); CK(s->alloc(&keys_s, G)); CK(s->alloc(&vals, G)); CK(s->alloc(&perm, G));
     CK(s->alloc(&scratch, 8)); CK(s->alloc(&err_idx, 1));
     const uint32_t init[8] = {0u, 0xffffffffu, 0u, 0xffffffffu, 0u, 0, 0, 0};  // err, min_u, max_u, min_v, max_v
@@ -648,7 +649,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
     if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
       return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
-    KL(launch_prep_norm(G, ru, rv, s->mm, gu_c, gv_c, st));
+    KL(launch_prep_norm(G, ru, rv, s->mm, din[0], din[1], din[2], kk, din[10], rec, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st));
     void* tmp = nullptr;
@@ -660,10 +661,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->gu, (size_t)s->G_pad));
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
     CK(s->alloc(&s->iperm, (size_t)G));
-    KL(launch_pack(G, s->G_pad, perm, din[0], din[1], din[2], kk, din[10], gu_c, gv_c, s->xy, s->zk, s->o2, s->gu,
-                   s->gv, s->iperm, st));
+    KL(launch_pack(G, s->G_pad, perm, rec, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, st));
     cudaFreeAsync(tmp, st);
-    s->release(ru); s->release(rv); s->release(kk); s->release(gu_c); s->release(gv_c);
+    s->release(ru); s->release(rv); s->release(kk); s->release(rec);
     s->release(keys); s->release(keys_s); s->release(vals); s->release(perm); s->release(scratch);
     s->release(err_idx);
     if (dev_in) s->release(dev_in);
@@ -696,6 +696,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaMemcpyAsync(s->cull, hcull.data(), sizeof(CullRow) * NL, cudaMemcpyHostToDevice, st));
     CK(s->alloc(&s->tile_lo, (size_t)s->n_tiles));
     CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
+    CK(s->alloc(&s->chunk_lo, (size_t)s->n_chunks));
+    CK(s->alloc(&s->chunk_hi, (size_t)s->n_chunks));
     CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
     CK(s->alloc(&s->kept, 1));
     KL(launch_tile_bounds(reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk), s->n_tiles,
@@ -711,7 +713,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
-    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
+    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
     // kept-camera lists per tile (CSR)
     unsigned long long kept_pairs = 0;
     CK(cudaMemcpyAsync(&kept_pairs, s->kept, sizeof(kept_pairs), cudaMemcpyDeviceToHost, st));
@@ -941,16 +943,18 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   }
   const int64_t W64 = (s->G + 63) / 64;
   const size_t bytes = (size_t)g.B * W64 * 8;
-  uint32_t *dc = nullptr, *de = nullptr;
+  uint32_t *dc = nullptr, *de = nullptr, *mt = nullptr;
   if (crop) CK(s->alloc(&dc, bytes / 4));
   if (eligible) CK(s->alloc(&de, bytes / 4));
+  CK(s->alloc(&mt, (size_t)g.B * s->words));
   CK(cudaEventRecord(s->ev[5], s->stream));
-  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, dc, de, s->stream));
+  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mt, dc, de, s->stream));
   CK(cudaEventRecord(s->ev[6], s->stream));
   TRY(copy_out(s, crop, dc, bytes));
   TRY(copy_out(s, eligible, de, bytes));
   s->release(dc);
   s->release(de);
+  s->release(mt);
   CK(cudaStreamSynchronize(s->stream));
   s->st.t_crop_ms = ms_between(s->ev[5], s->ev[6]);
   return LOBE_OK;

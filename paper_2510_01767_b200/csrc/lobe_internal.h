@@ -59,14 +59,14 @@ struct PrepIn {
 cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* keys, int32_t* vals,
                             uint32_t* err, unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
 // Normalise the ground coordinates to [0,1].
-cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, float* gu, float* gv,
+cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, const float* x,
+                             const float* y, const float* z, const float* kk, const float* o, float4* rec,
                              cudaStream_t st);
 cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                              int32_t* vout, int64_t n, cudaStream_t st);
 // Gather into the internal pair-interleaved layout, build the inverse permutation.
-cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float* x, const float* y,
-                        const float* z, const float* kk, const float* o, const float* gu_c, const float* gv_c,
-                        float* xy, float* zk, float* o2, float* gu, float* gv, int32_t* iperm, cudaStream_t st);
+cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float4* rec, float* xy, float* zk,
+                        float* o2, float* gu, float* gv, int32_t* iperm, cudaStream_t st);
 
 // a3: visibility tests -> rows, tile flags, per-(chunk,camera) partials.
 struct VisArgs {
@@ -92,8 +92,10 @@ struct CullRow {
 };
 cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_tiles, float4* tlo, float4* thi,
                                cudaStream_t st);
-cudaError_t launch_cull(const float4* tlo, const float4* thi, int64_t n_tiles, const CullRow* rows, int64_t n_cams,
-                        uint32_t* keep, unsigned long long* kept_pairs, cudaStream_t st);
+// hierarchical: chunk boxes (clo/chi scratch, n_tiles/16 each) then tile boxes
+cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float4* chi, int64_t n_tiles,
+                        const CullRow* rows, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
+                        cudaStream_t st);
 // kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
                               const uint32_t* offs, uint32_t* list, int phase, cudaStream_t st);
@@ -123,8 +125,8 @@ cudaError_t launch_tile_fill(const uint8_t* flags, int64_t n_tiles, int64_t n_ca
                              uint32_t* pair_cam, uint32_t* pair_tile, cudaStream_t st);
 
 // a5: per-Gaussian zone pair, per-word / per-tile uniform zone, per-zone counts.
-cudaError_t launch_zones(const ZoneTables* dz, int nzv, int64_t G, int64_t G_pad, const float* gu, const float* gv,
-                         uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone, uint32_t* zp_count,
+cudaError_t launch_zones(const ZoneTables* dz, int nzv, int nzp, int64_t G, int64_t G_pad, const float* gu,
+                         const float* gv, uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone, uint32_t* zp_count,
                          cudaStream_t st);
 // a6: zone-pair histograms per camera from the (tile, camera) pairs.
 cudaError_t launch_hist(int64_t n_pairs, const uint32_t* pair_cam, const uint32_t* pair_tile, const uint32_t* rows,
@@ -157,8 +159,9 @@ cudaError_t launch_block_masks(int64_t n_tiles, const uint32_t* tile_off, const 
 cudaError_t launch_masks_combine(const uint32_t* gathered, int W, int B, int64_t words, uint32_t* out,
                                  uint32_t* gvis, cudaStream_t st);
 // a9: caller-order crop / eligible masks.
+// mt: scratch, B x words u32 (word-major transpose of masks)
 cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint8_t* zp_cellblock,
-                        const uint32_t* masks, int64_t words, int B, uint32_t* crop32, uint32_t* elig32,
+                        const uint32_t* masks, int64_t words, int B, uint32_t* mt, uint32_t* crop32, uint32_t* elig32,
                         cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
                                int64_t count, const uint8_t* flags, int64_t n_cams, uint32_t* out, cudaStream_t st);
