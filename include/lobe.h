@@ -161,7 +161,8 @@ typedef struct {
   uint64_t tile_pairs; /* (tile, camera) pairs with any visible Gaussian */
   uint64_t dense_tests;     /* tests evaluated densely in the last visibility pass (tile culling skips the
                                rest, each proven invisible: SURVEY §8f NEXT-3); logical tests = G x N_local */
-  double t_cull_ms;         /* tile-culling pre-pass of the last visibility pass (inside t_vis_ms) */
+  double t_cull_ms;         /* tile-culling kernel of the last visibility pass (included in t_vis_ms,
+                               which is culling + test kernels) */
   double t_depth_ms;        /* depth statistic over the non-empty (tile, camera) pairs (a4) */
   uint64_t kernel_launches; /* cumulative launches of this library's own kernels */
   uint64_t cub_launches;    /* cumulative CUB primitive calls (radix sort, scan) */

@@ -140,7 +140,7 @@ struct lobe_scene {
   unsigned long long h_incid[kMaxBlocks];
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[12] = {};
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -714,6 +714,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
     if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
+    CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
     unsigned long long kept_pairs = 0;
     CK(cudaMemcpyAsync(&kept_pairs, s->kept, sizeof(kept_pairs), cudaMemcpyDeviceToHost, st));
@@ -758,7 +759,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     s->release(uc);
     s->release(uoff);
-    CK(cudaEventRecord(s->ev[7], st));
+    CK(cudaEventRecord(s->ev[9], st));
     if (s->N_loc > 0 && kept_pairs > 0) {
       VisArgs va{};
       va.xy = reinterpret_cast<const float4*>(s->xy);
@@ -775,6 +776,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
+    CK(cudaEventRecord(s->ev[10], st));
     CK(cudaEventRecord(s->ev[2], st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
@@ -849,8 +851,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaEventRecord(s->ev[3], st));
     CK(cudaStreamSynchronize(st));
     s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
-    s->st.t_vis_ms = ms_between(s->ev[1], s->ev[2]);
-    s->st.t_cull_ms = ms_between(s->ev[1], s->ev[7]);
+    // visibility pass = culling kernel + test kernel (list building excluded)
+    s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
+    s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
     s->st.t_depth_ms = ms_between(s->ev[4], s->ev[5]);
     s->st.dense_tests = (uint64_t)kept_pairs * (uint64_t)kTile;
     s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;

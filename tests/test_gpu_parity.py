@@ -289,3 +289,52 @@ def test_errors_gpu():
             S.block_loads(9, 9)
         assert e.value.status == "INVALID_CONFIG"
         S.block_loads(2, 2)   # handle still valid after failures
+
+
+def _fuzz_scene(seed, G=6000, N=24):
+    """Adversarial geometry for the tile culling: Gaussians in a box that the
+    cameras sit inside (camera planes cut through tiles, points behind and
+    beside every camera), heavy-tailed scales (huge footprints), some gated,
+    random intrinsics and depth ranges."""
+    from synth.scenes import Scene, SceneConfig
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: np.asarray(a, dtype=np.float32)
+    mu = rng.uniform(-1, 1, size=(G, 3))
+    mu[: G // 4] *= rng.uniform(0.0, 0.02, size=(G // 4, 1))      # a dense blob at the origin
+    s = np.exp(rng.normal(np.log(0.01), 1.5, size=(G, 3)))
+    q = rng.normal(size=(G, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    op = rng.uniform(0, 1, G)
+    op[rng.uniform(size=G) < 0.1] = 0.001                            # gated
+    cams = []
+    for c in range(N):
+        p = rng.uniform(-0.8, 0.8, 3)
+        f = rng.normal(size=3)
+        f /= np.linalg.norm(f)
+        up = np.array([0.0, 0.0, 1.0]) if abs(f[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+        xa = np.cross(f, up)
+        xa /= np.linalg.norm(xa)
+        ya = np.cross(f, xa)
+        R = np.stack([xa, ya, f])
+        W, H = int(rng.integers(32, 400)), int(rng.integers(32, 400))
+        fx = float(rng.uniform(0.3, 2.0) * W)
+        fy = float(fx * rng.uniform(0.8, 1.25))
+        zn = float(10 ** rng.uniform(-3, -1))
+        cams.append(dict(R=R, t=-R @ p, W=W, H=H, fx=fx, fy=fy, cx=W * rng.uniform(0.3, 0.7),
+                         cy=H * rng.uniform(0.3, 0.7), zn=zn, zf=float(zn * 10 ** rng.uniform(1, 4))))
+    cfg = SceneConfig("fuzz", G, N, 3, 2, 100, 100, 60.0, (-1, 1, -1, 1), 1.0, 1, 0.0, seed)
+    return Scene(cfg, f32(mu[:, 0]), f32(mu[:, 1]), f32(mu[:, 2]), f32(s[:, 0]), f32(s[:, 1]), f32(s[:, 2]),
+                 f32(q[:, 0]), f32(q[:, 1]), f32(q[:, 2]), f32(q[:, 3]), f32(op),
+                 cam_id=np.arange(N, dtype=np.int32), fx=f32([c["fx"] for c in cams]), fy=f32([c["fy"] for c in cams]),
+                 cx=f32([c["cx"] for c in cams]), cy=f32([c["cy"] for c in cams]),
+                 width=np.array([c["W"] for c in cams], np.int32), height=np.array([c["H"] for c in cams], np.int32),
+                 R=f32([c["R"] for c in cams]), t=f32([c["t"] for c in cams]),
+                 z_near=f32([c["zn"] for c in cams]), z_far=f32([c["zf"] for c in cams]))
+
+
+@pytest.mark.parametrize("seed,G", [(1, 6000), (2, 6000), (3, 50_000), (4, 50_000)])
+def test_fuzz_culling_exact(seed, G):
+    """Tile culling never drops a visible Gaussian (and the whole path stays
+    bit-exact) under adversarial camera placement and footprints."""
+    sc = _fuzz_scene(seed, G=G)
+    full_parity(sc, [oracle.default_grid(3, 2), _rand_grid(4, 4, seed)])
