@@ -217,7 +217,7 @@ def main():
     elig_d = torch.empty(B * W64, dtype=torch.int64, device="cuda")
     group = None
     stats_acc = {"t_vis_ms": [], "t_cull_ms": [], "t_depth_ms": [], "kernels": 0, "cub": 0, "tests": 0,
-                 "dense": 0, "pairs": 0}
+                 "dense": 0, "pairs": 0, "kept": 0, "accepted": 0}
 
     def step(gsrc, crop_out, elig_out):
         eng = Engine.from_scene(gsrc, cams, stream=stream, group=group)
@@ -229,6 +229,8 @@ def main():
         stats_acc["t_cull_ms"].append(st.t_cull_ms)
         stats_acc["t_depth_ms"].append(st.t_depth_ms)
         stats_acc["dense"] = st.dense_tests
+        stats_acc["kept"] = st.kept_tests
+        stats_acc["accepted"] = st.accepted_tests
         stats_acc["kernels"] += st.kernel_launches
         stats_acc["cub"] += st.cub_launches
         stats_acc["tests"] += st.tests_executed
@@ -269,6 +271,7 @@ def main():
     t_cull = statistics.mean(stats_acc["t_cull_ms"])
     t_depth = statistics.mean(stats_acc["t_depth_ms"])
     dense_tests = stats_acc["dense"]
+    kept_tests, accepted_tests = stats_acc["kept"], stats_acc["accepted"]
     timed_kernels, timed_cub = stats_acc["kernels"], stats_acc["cub"]
     n_local = N // world if world > 1 else N
     value = G * N / (ms * 1e-3)
@@ -321,8 +324,9 @@ def main():
         pass
     sm_max_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     peak = sms * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12  # TFLOP/s
-    # roofline on the EXECUTED tests (tile culling skips tests proven invisible;
-    # "the roofline stays defined on executed tests")
+    # roofline on the EXECUTED exact tests: box bounds decide the rest (tile and
+    # slice rejections, slice acceptances; "the roofline stays
+    # defined on executed tests")
     achieved = FLOP_PER_TEST * dense_tests / (t_vis * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_visibility_traffic.json")
@@ -334,13 +338,16 @@ def main():
         except Exception:
             pass
     clocks = clk.summary()
-    roof = {"bound": "alu", "kernel": "k_cull + k_vis (a3)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": "alu", "kernel": "k_cull + k_vis_tiles (a3)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max_mhz:.0f} MHz "
                           "(sm_max_mhz of MEASURED_PEAKS.json); 22 flop/test",
             "kernel_ms": t_vis, "cull_ms": t_cull, "kernel_share_of_step": t_vis / ms,
             "executed_tests": int(dense_tests), "logical_tests": int(G * n_local),
             "executed_fraction": dense_tests / float(G * n_local),
+            "decided_by_bounds": {"tile_rejected": int(G * n_local - kept_tests),
+                                  "slice_rejected": int(kept_tests - dense_tests - accepted_tests),
+                                  "slice_accepted": int(accepted_tests)},
             "logical_tests_per_s_kernel": G * n_local / (t_vis * 1e-3),
             "executed_tests_per_s_kernel": dense_tests / (t_vis * 1e-3),
             "depth_stat_ms": t_depth,

@@ -159,13 +159,17 @@ typedef struct {
   uint64_t vis_launches, evaluations;
   int64_t n_gaussians, n_cameras, n_local_cameras, cam_begin;
   uint64_t tile_pairs; /* (tile, camera) pairs with any visible Gaussian */
-  uint64_t dense_tests;     /* tests evaluated densely in the last visibility pass (tile culling skips the
-                               rest, each proven invisible: SURVEY §8f NEXT-3); logical tests = G x N_local */
+  uint64_t dense_tests;     /* exact per-Gaussian tests run in the last visibility pass; the other logical
+                               tests (G x N_local) are decided by box bounds:
+                               rejected tiles/slices (no Gaussian visible) or accepted slices (every
+                               non-gated Gaussian visible) -- identical results, see k_vis_tiles */
   double t_cull_ms;         /* tile-culling kernel of the last visibility pass (included in t_vis_ms,
                                which is culling + test kernels) */
   double t_depth_ms;        /* depth statistic over the non-empty (tile, camera) pairs (a4) */
   uint64_t kernel_launches; /* cumulative launches of this library's own kernels */
   uint64_t cub_launches;    /* cumulative CUB primitive calls (radix sort, scan) */
+  uint64_t kept_tests;      /* tests in (tile, camera) pairs the tile bound did not reject (last pass) */
+  uint64_t accepted_tests;  /* tests in (slice, camera) pairs the slice bound accepted (last pass) */
 } lobe_stats;
 
 /* ---- scene --------------------------------------------------------------- */

@@ -102,7 +102,8 @@ struct lobe_scene {
   uint32_t* cam_off = nullptr;
   int32_t* cam_order = nullptr;
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
-  CullRow* cull = nullptr;
+  float4 *slice_lo = nullptr, *slice_hi = nullptr;
+  unsigned long long* vcnt = nullptr;  // k_vis_tiles counters: undecided, accepted
   uint32_t* keep = nullptr;
   unsigned long long* kept = nullptr;
   uint32_t *koff = nullptr, *klist = nullptr, *unit_tile = nullptr;
@@ -244,23 +245,6 @@ CamSetup camera_setup(const lobe_camera& k) {
   s.zn = k.z_near;
   s.zf = k.z_far;
   return s;
-}
-
-// Tile-culling forms (fp64 of the fp32 setup): w, u, v, eu = u - Wf w, ev = v - Hf w.
-CullRow cull_row(const CamSetup& c) {
-  CullRow r{};
-  for (int i = 0; i < 4; ++i) {
-    r.f[0][i] = c.Aw[i];
-    r.f[1][i] = c.Au[i];
-    r.f[2][i] = c.Av[i];
-    r.f[3][i] = (double)c.Au[i] - (double)c.Wf * (double)c.Aw[i];
-    r.f[4][i] = (double)c.Av[i] - (double)c.Hf * (double)c.Aw[i];
-  }
-  r.zn = c.zn;
-  r.zf = c.zf;
-  r.Wf = c.Wf;
-  r.Hf = c.Hf;
-  return r;
 }
 
 // O3's fp32 map for one point (contraction + ground projection), host side.
@@ -525,7 +509,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cull); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -670,13 +654,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
 
     // ---- a2 camera setup (local shard) + camera-centre grid coords
     std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
-    std::vector<CullRow> hcull(std::max<int64_t>(s->N_loc, 1));
     s->cam_gu.assign(s->N_loc, 0.f);
     s->cam_gv.assign(s->N_loc, 0.f);
     for (int64_t c = 0; c < s->N_loc; ++c) {
       const lobe_camera& k = cams[s->cam_begin + c];
       hset[c] = camera_setup(k);
-      hcull[c] = cull_row(hset[c]);
       double oc[3];
       cam_centre(k, oc);
       float ru_, rv_;
@@ -692,16 +674,17 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->d_cam_gv, NL));
     CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, st));
     s->n_sub = (NL + 31) / 32;
-    CK(s->alloc(&s->cull, NL));
-    CK(cudaMemcpyAsync(s->cull, hcull.data(), sizeof(CullRow) * NL, cudaMemcpyHostToDevice, st));
     CK(s->alloc(&s->tile_lo, (size_t)s->n_tiles));
     CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
+    CK(s->alloc(&s->slice_lo, (size_t)s->n_tiles * 4));
+    CK(s->alloc(&s->slice_hi, (size_t)s->n_tiles * 4));
+    CK(s->alloc(&s->vcnt, 2));
     CK(s->alloc(&s->chunk_lo, (size_t)s->n_chunks));
     CK(s->alloc(&s->chunk_hi, (size_t)s->n_chunks));
     CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
     CK(s->alloc(&s->kept, 1));
     KL(launch_tile_bounds(reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk), s->n_tiles,
-                          s->tile_lo, s->tile_hi, st));
+                          s->tile_lo, s->tile_hi, s->slice_lo, s->slice_hi, st));
     if (s->N_loc > 0) {
       CK(cudaMemcpyAsync(s->d_cam_gu, s->cam_gu.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(s->d_cam_gv, s->cam_gv.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
@@ -713,7 +696,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
-    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cull, s->N_loc, s->keep, s->kept, st));
+    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->N_loc, s->keep, s->kept, st));
     CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
     unsigned long long kept_pairs = 0;
@@ -759,6 +742,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     s->release(uc);
     s->release(uoff);
+    CK(cudaMemsetAsync(s->vcnt, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaEventRecord(s->ev[9], st));
     if (s->N_loc > 0 && kept_pairs > 0) {
       VisArgs va{};
@@ -773,10 +757,15 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.flags = s->flags;
       va.keep = s->keep;
       va.n_sub = s->n_sub;
+      va.slo = s->slice_lo;
+      va.shi = s->slice_hi;
+      va.counters = s->vcnt;
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[10], st));
+    unsigned long long vc[2] = {0, 0};
+    CK(cudaMemcpyAsync(vc, s->vcnt, sizeof(vc), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(s->ev[2], st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
@@ -855,7 +844,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
     s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
     s->st.t_depth_ms = ms_between(s->ev[4], s->ev[5]);
-    s->st.dense_tests = (uint64_t)kept_pairs * (uint64_t)kTile;
+    s->st.kept_tests = (uint64_t)kept_pairs * (uint64_t)kTile;  // pairs surviving the tile bound
+    s->st.dense_tests = (uint64_t)vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
+    s->st.accepted_tests = (uint64_t)vc[1] * (uint64_t)(kTile / 4);
     s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
     s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
     s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
@@ -1042,6 +1033,9 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.flags = s->flags;
   va.keep = s->keep;
   va.n_sub = s->n_sub;
+  va.slo = s->slice_lo;
+  va.shi = s->slice_hi;
+  va.counters = nullptr;
   int g = 0;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)

@@ -81,20 +81,20 @@ struct VisArgs {
   uint8_t* flags;      // [n_tiles x n_cams], zeroed before the pass; 1 = some Gaussian visible
   const uint32_t* keep;  // [n_tiles x n_sub] camera masks surviving tile culling (NULL: dense)
   int64_t n_sub;         // ceil(n_cams / 32)
+  const float4* slo;     // [n_tiles x 4] slice boxes (256 Gaussians) for k_vis_tiles
+  const float4* shi;
+  unsigned long long* counters;  // k_vis_tiles: [0] undecided, [1] accepted (slice, camera) pairs; may be NULL
 };
 
 // Tile culling: per camera the five linear forms of the
 // test (w, u, v, eu, ev as c . p + c0, fp64 from the fp32 setup) and the depth
 // range; per tile the AABB of its non-gated Gaussian centres and max k.
-struct CullRow {
-  double f[5][4];  // w, u, v, eu, ev: {c_x, c_y, c_z, c_0}
-  float zn, zf, Wf, Hf;
-};
+// tile boxes and 256-Gaussian slice boxes: lo = {x, y, z, kmin}, hi = {x, y, z, kmax}
 cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_tiles, float4* tlo, float4* thi,
-                               cudaStream_t st);
+                               float4* slo, float4* shi, cudaStream_t st);
 // hierarchical: chunk boxes (clo/chi scratch, n_tiles/16 each) then tile boxes
 cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float4* chi, int64_t n_tiles,
-                        const CullRow* rows, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
+                        const CamSetup* cams, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
                         cudaStream_t st);
 // kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,

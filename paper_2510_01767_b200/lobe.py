@@ -82,7 +82,8 @@ class Stats(ctypes.Structure):
                [("tile_pairs", ctypes.c_uint64), ("dense_tests", ctypes.c_uint64), ("t_cull_ms", ctypes.c_double),
                 ("t_depth_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_uint64),
-                ("cub_launches", ctypes.c_uint64)]
+                ("cub_launches", ctypes.c_uint64), ("kept_tests", ctypes.c_uint64),
+                ("accepted_tests", ctypes.c_uint64)]
 
 
 OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),

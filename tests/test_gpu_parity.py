@@ -60,6 +60,7 @@ def full_parity(sc, grids, mode=0):
         assert (S.frame["center"] == c0).all() and S.frame["radius"] == rho
         rows = S.export_rows()
         assert (rows == o0["vis"]["rows"]).all()
+        st = S.stats()
         for g in grids:
             o = o0 if g is grids[0] else None
             if o is None:
@@ -74,6 +75,7 @@ def full_parity(sc, grids, mode=0):
             _cmp_loads(L, bl)
             c, e = S.crop_masks(g["m"], g["n"], **_grid_kw(g))
             assert (c == cr).all() and (e == el).all()
+    return st
 
 
 def _rand_grid(m, n, seed, **kw):
@@ -338,3 +340,78 @@ def test_fuzz_culling_exact(seed, G):
     bit-exact) under adversarial camera placement and footprints."""
     sc = _fuzz_scene(seed, G=G)
     full_parity(sc, [oracle.default_grid(3, 2), _rand_grid(4, 4, seed)])
+
+
+def _edge_scene(seed, N=16, clusters=12, per=300):
+    """Tight clusters (radius 1e-4 of the depth) placed just inside and just
+    outside every frustum boundary of every camera -- the four image edges
+    dilated by the footprint, the near and the far plane -- so that 256-Gaussian
+    slice boxes land on both sides of each condition. Exercises the slice
+    accept / reject bounds of k_vis_tiles against the exact test."""
+    from synth.scenes import Scene, SceneConfig
+    rng = np.random.default_rng(1000 + seed)
+    f32 = lambda a: np.asarray(a, dtype=np.float32)
+    cams = []
+    for c in range(N):
+        p = rng.uniform(-0.5, 0.5, 3)
+        f = rng.normal(size=3)
+        f /= np.linalg.norm(f)
+        up = np.array([0.0, 0.0, 1.0]) if abs(f[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+        xa = np.cross(f, up)
+        xa /= np.linalg.norm(xa)
+        ya = np.cross(f, xa)
+        R = np.stack([xa, ya, f])
+        W, H = int(rng.integers(64, 400)), int(rng.integers(64, 400))
+        fx = float(rng.uniform(0.5, 2.0) * W)
+        fy = float(fx * rng.uniform(0.8, 1.25))
+        zn = float(10 ** rng.uniform(-2, -1))
+        cams.append(dict(R=R, p=p, t=-R @ p, W=W, H=H, fx=fx, fy=fy, cx=W * rng.uniform(0.3, 0.7),
+                         cy=H * rng.uniform(0.3, 0.7), zn=zn, zf=float(zn * 10 ** rng.uniform(1, 2))))
+    pts, scl = [], []
+    for cam in cams:
+        for k in range(clusters):
+            side = k % 6  # 0..3 image edges, 4 near plane, 5 far plane
+            z = rng.uniform(1.5 * cam["zn"], 0.7 * cam["zf"])
+            px, py = rng.uniform(0, cam["W"]), rng.uniform(0, cam["H"])
+            off = (1 if rng.uniform() < 0.5 else -1) * 10 ** rng.uniform(-3, 1)  # pixels / depth units
+            if side == 0:
+                px = 0.0 + off
+            elif side == 1:
+                px = cam["W"] + off
+            elif side == 2:
+                py = 0.0 + off
+            elif side == 3:
+                py = cam["H"] + off
+            elif side == 4:
+                z = cam["zn"] * (1 + off * 1e-2)
+            else:
+                z = cam["zf"] * (1 + off * 1e-2)
+            xc = np.array([(px - cam["cx"]) / cam["fx"] * z, (py - cam["cy"]) / cam["fy"] * z, z])
+            centre = cam["R"].T @ xc + cam["p"]
+            pts.append(centre + rng.normal(scale=1e-4 * z, size=(per, 3)))
+            scl.append(np.full((per, 3), 10 ** rng.uniform(-7, -4)))
+    mu = np.concatenate(pts)
+    s = np.concatenate(scl) * np.exp(rng.normal(0, 0.3, size=(len(mu), 3)))
+    G = len(mu)
+    q = rng.normal(size=(G, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    op = rng.uniform(0.01, 1, G)
+    op[rng.uniform(size=G) < 0.05] = 0.001
+    cfg = SceneConfig("edge", G, N, 2, 2, 100, 100, 60.0, (-1, 1, -1, 1), 1.0, 1, 0.0, seed)
+    return Scene(cfg, f32(mu[:, 0]), f32(mu[:, 1]), f32(mu[:, 2]), f32(s[:, 0]), f32(s[:, 1]), f32(s[:, 2]),
+                 f32(q[:, 0]), f32(q[:, 1]), f32(q[:, 2]), f32(q[:, 3]), f32(op),
+                 cam_id=np.arange(N, dtype=np.int32), fx=f32([c["fx"] for c in cams]), fy=f32([c["fy"] for c in cams]),
+                 cx=f32([c["cx"] for c in cams]), cy=f32([c["cy"] for c in cams]),
+                 width=np.array([c["W"] for c in cams], np.int32), height=np.array([c["H"] for c in cams], np.int32),
+                 R=f32([c["R"] for c in cams]), t=f32([c["t"] for c in cams]),
+                 z_near=f32([c["zn"] for c in cams]), z_far=f32([c["zf"] for c in cams]))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_edge_clusters_exact(seed):
+    """Slice bounds (accept / reject) never change a test outcome: clusters
+    straddling every frustum boundary, compared in full with the oracle; the
+    scene must actually exercise accepted, rejected and exact slices."""
+    sc = _edge_scene(seed)
+    st = full_parity(sc, [oracle.default_grid(2, 2)])
+    assert st.accepted_tests > 0 and st.dense_tests > 0 and st.kept_tests > st.dense_tests + st.accepted_tests
