@@ -380,7 +380,7 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
   if (s->N_loc > 0) {
     CK(cudaMemsetAsync(s->hist, 0, sizeof(uint32_t) * (size_t)s->N_loc * nzp, st));
-    KL(launch_hist(s->n_pairs, s->pair_cam, s->pair_tile, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
+    KL(launch_hist(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
                    s->hist, st));
   }
   CK(cudaEventRecord(s->ev[3], st));

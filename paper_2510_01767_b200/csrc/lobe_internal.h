@@ -129,7 +129,8 @@ cudaError_t launch_zones(const ZoneTables* dz, int nzv, int nzp, int64_t G, int6
                          const float* gv, uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone, uint32_t* zp_count,
                          cudaStream_t st);
 // a6: zone-pair histograms per camera from the (tile, camera) pairs.
-cudaError_t launch_hist(int64_t n_pairs, const uint32_t* pair_cam, const uint32_t* pair_tile, const uint32_t* rows,
+// a6 per (tile, batch of 32 cameras of the tile's non-empty list)
+cudaError_t launch_hist(int64_t n_tiles, const uint32_t* tile_off, const uint32_t* pair_cam, const uint32_t* rows,
                         int64_t words, const uint16_t* zp, const uint16_t* word_zone, const uint16_t* tile_zone,
                         int nzp, uint32_t* hist, cudaStream_t st);
 // a7: n, n0, member, home, selection mask, |C^(b)|, I_b.
