@@ -351,6 +351,11 @@ def main():
             "logical_tests_per_s_kernel": G * n_local / (t_vis * 1e-3),
             "executed_tests_per_s_kernel": dense_tests / (t_vis * 1e-3),
             "depth_stat_ms": t_depth,
+            # roofline time of the dense pass = 22 flop x G x N / peak; the
+            # target (>= 60 % of it) is >= 0.6 x peak / 22 logical tests/s
+            "dense_roofline_ms": FLOP_PER_TEST * G * n_local / (peak * 1e12) * 1e3,
+            "logical_frac_of_dense_roofline": (FLOP_PER_TEST * G * n_local / (peak * 1e12) * 1e3) / t_vis,
+            "target_logical_tests_per_s": 0.6 * peak * 1e12 / FLOP_PER_TEST,
             "frac_at_measured_clock": (achieved / (peak * (clocks["sm_mhz"] or sm_max_mhz) / sm_max_mhz))}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
