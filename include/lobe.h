@@ -248,6 +248,13 @@ lobe_status lobe_crop_from_masks(lobe_scene* scene, const lobe_grid* grid, const
 
 /* ---- introspection / tests ----------------------------------------------- */
 
+/* Sizes of a loaded scene without waiting for its work to finish (lobe_get_stats
+ * synchronises the scene's stream to read the load-pass timings): total
+ * Gaussians and cameras, this rank's camera count and first camera. Any output
+ * pointer may be NULL. Errors: LOBE_E_STATE if s is NULL. */
+lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* n_cameras, int64_t* n_local_cameras,
+                            int64_t* cam_begin);
+
 /* Visibility rows of local cameras [c0, c0 + count) in caller Gaussian order:
  * count x ceil(G/32) u32, bit (i mod 32) of word i/32 (for parity tests). */
 lobe_status lobe_export_rows(lobe_scene* scene, int64_t c0, int64_t count, uint32_t* rows);

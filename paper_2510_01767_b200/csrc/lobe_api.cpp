@@ -9,11 +9,13 @@
 // coordinates, region bounds) are single IEEE operations in the order written.
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <limits>
 #include <string>
 #include <vector>
+#include <mutex>
 
 #include <functional>
 
@@ -137,11 +139,28 @@ struct lobe_scene {
   double ev_tau = 0;
   ZoneTables hz{};
   std::vector<uint8_t> zp_cell;
-  uint32_t h_ncams[kMaxBlocks], h_gvis[kMaxBlocks], h_gblk[kMaxBlocks];
-  unsigned long long h_incid[kMaxBlocks];
+  // pinned host staging (asynchronous copies; one synchronisation per call)
+  struct Pinned {
+    ZoneTables Z;
+    uint8_t zp_cell[kMaxZones * kMaxZones];
+    alignas(16) uint32_t counts[3 * kMaxBlocks];  // mirrors the device block: ncams, gvis, gblk
+    unsigned long long incid[kMaxBlocks];   // then incid (contiguous on the device too)
+    unsigned long long vc[2];               // k_vis_tiles counters of the last pass
+  };
+  static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
+                "pinned counts / incid must mirror the contiguous device block");
+  Pinned* pin = nullptr;
+  uint8_t* pin_out = nullptr;  // growable staging for per-camera outputs
+  size_t pin_out_cap = 0;
+  bool stats_pending = false;  // load-pass timings read lazily (lobe_get_stats)
+  unsigned long long kept_pairs_last = 0;
+  const uint32_t* h_ncams() const { return pin->counts; }
+  const uint32_t* h_gvis() const { return pin->counts + kMaxBlocks; }
+  const uint32_t* h_gblk() const { return pin->counts + 2 * kMaxBlocks; }
+  const unsigned long long* h_incid() const { return pin->incid; }
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[14] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4; crop / comm: 5, 6; dev bench: 6, 7
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -368,11 +387,13 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   s->hz = Z;
   s->zp_cell.assign(nzp, 0);
   for (int zp = 0; zp < nzp; ++zp) s->zp_cell[zp] = (uint8_t)(Z.U.cell[zp / nzv] * g.n + Z.V.cell[zp % nzv]);
-  CK(cudaMemcpyAsync(s->dz, &Z, sizeof(Z), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(s->d_zp_cell, s->zp_cell.data(), nzp, cudaMemcpyHostToDevice, st));
+  s->pin->Z = Z;
+  std::memcpy(s->pin->zp_cell, s->zp_cell.data(), nzp);
+  CK(cudaMemcpyAsync(s->dz, &s->pin->Z, sizeof(Z), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->d_zp_cell, s->pin->zp_cell, nzp, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(s->zp_count, 0, sizeof(uint32_t) * kMaxZones * kMaxZones, st));
-  CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks, st));
-  CK(cudaMemsetAsync(s->incid, 0, sizeof(unsigned long long) * kMaxBlocks, st));
+  // counts [3 x kMaxBlocks] u32 and incid [kMaxBlocks] u64 are one device block
+  CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks, st));
   CK(cudaEventRecord(s->ev[2], st));
   KL(launch_zones(s->dz, nzv, nzp, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
   KL(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
@@ -411,11 +432,9 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
                           s->counts + kMaxBlocks, st));
   }
   CK(cudaEventRecord(s->ev[4], st));
-  CK(cudaMemcpyAsync(s->h_ncams, s->counts, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(s->h_gvis, s->counts + kMaxBlocks, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(s->h_gblk, s->counts + 2 * kMaxBlocks, sizeof(uint32_t) * kMaxBlocks, cudaMemcpyDeviceToHost,
-                     st));
-  CK(cudaMemcpyAsync(s->h_incid, s->incid, sizeof(unsigned long long) * kMaxBlocks, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s->pin->counts, s->counts,
+                     sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks,
+                     cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   s->st.t_hist_ms = ms_between(s->ev[2], s->ev[3]);
   s->st.t_loads_ms = ms_between(s->ev[3], s->ev[4]);
@@ -474,7 +493,7 @@ void fill_records(const lobe_scene* s, const GridV& g, const uint32_t* ncams, co
     r.hi[1] = vehi[q];
     r.area = ((double)uhi[p] - (double)ulo[p]) * ((double)vhi[q] - (double)vlo[q]);
     r.n_cams = ncams[b];
-    r.g_blk = s->h_gblk[b];
+    r.g_blk = s->h_gblk()[b];
     r.g_vis = gvis[b];
     r.g_avgvis = r.n_cams ? (double)r.g_vis / (double)r.n_cams : 0.0;
     r.incidences = incid[b];
@@ -482,6 +501,101 @@ void fill_records(const lobe_scene* s, const GridV& g, const uint32_t* ncams, co
     if (out) out[b] = r;
   }
   if (objective) *objective = best;
+}
+
+// Load-pass timings and counters (events and pinned counters of the last load).
+void finalize_load_stats(lobe_scene* s) {
+  if (!s->stats_pending) return;
+  cudaStreamSynchronize(s->stream);
+  s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
+  // visibility pass = culling kernel + test kernel (list building excluded)
+  s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
+  s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
+  s->st.t_depth_ms = ms_between(s->ev[11], s->ev[12]);
+  s->st.kept_tests = (uint64_t)s->kept_pairs_last * (uint64_t)kTile;  // pairs surviving the tile bound
+  s->st.dense_tests = (uint64_t)s->pin->vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
+  s->st.accepted_tests = (uint64_t)s->pin->vc[1] * (uint64_t)(kTile / 4);
+  s->stats_pending = false;
+}
+
+// Pinned staging blocks, recycled across scenes (cudaFreeHost would synchronise).
+std::mutex g_pin_mu;
+std::vector<void*> g_pin_free;
+lobe_scene::Pinned* acquire_pinned() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      void* p = g_pin_free.back();
+      g_pin_free.pop_back();
+      return static_cast<lobe_scene::Pinned*>(p);
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, sizeof(lobe_scene::Pinned)) != cudaSuccess) return nullptr;
+  return static_cast<lobe_scene::Pinned*>(p);
+}
+void recycle_pinned(lobe_scene::Pinned* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+std::vector<std::pair<uint8_t*, size_t>> g_pin_out_free;
+uint8_t* acquire_pinned_out(size_t need, size_t* cap) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_pin_out_free.size(); ++i)
+      if (g_pin_out_free[i].second >= need) {
+        auto e = g_pin_out_free[i];
+        g_pin_out_free.erase(g_pin_out_free.begin() + i);
+        *cap = e.second;
+        return e.first;
+      }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, need) != cudaSuccess) return nullptr;
+  *cap = need;
+  return static_cast<uint8_t*>(p);
+}
+void recycle_pinned_out(uint8_t* p, size_t cap) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_out_free.emplace_back(p, cap);
+}
+
+// Per-camera outputs: asynchronous copies into pinned staging when the
+// destination is ordinary pageable host memory, one synchronisation, then host
+// copies into the caller's buffers (out_plan collects them).
+struct StagedCopy { void* dst; size_t off, bytes; };
+lobe_status stage_out(lobe_scene* s, std::vector<StagedCopy>& plan, size_t& used, void* dst, const void* src,
+                      size_t bytes) {
+  if (!dst || bytes == 0) return LOBE_OK;
+  cudaPointerAttributes at{};
+  const bool pageable = cudaPointerGetAttributes(&at, dst) != cudaSuccess || at.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();  // clear a possible error of the attribute query
+  if (!pageable) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->stream));
+    return LOBE_OK;
+  }
+  plan.push_back(StagedCopy{dst, used, bytes});
+  used += (bytes + 15) & ~size_t(15);
+  return LOBE_OK;
+}
+lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used,
+                       const std::vector<const void*>& srcs) {
+  if (used > s->pin_out_cap) {
+    CK(cudaStreamSynchronize(s->stream));  // the old block may still be a copy target
+    recycle_pinned_out(s->pin_out, s->pin_out_cap);
+    s->pin_out = acquire_pinned_out(used, &s->pin_out_cap);
+    if (!s->pin_out) {
+      s->pin_out_cap = 0;
+      return fail(LOBE_E_CUDA, "pinned staging allocation failed");
+    }
+  }
+  for (size_t i = 0; i < plan.size(); ++i)
+    CK(cudaMemcpyAsync(s->pin_out + plan[i].off, srcs[i], plan[i].bytes, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  for (const auto& c : plan) std::memcpy(c.dst, s->pin_out + c.off, c.bytes);
+  return LOBE_OK;
 }
 
 lobe_status copy_out(lobe_scene* s, void* dst, const void* src, size_t bytes) {
@@ -515,10 +629,12 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
   s->release(s->ncb); s->release(s->n0cb); s->release(s->member); s->release(s->sel); s->release(s->home);
-  s->release(s->counts); s->release(s->incid); s->release(s->masks);
+  s->release(s->counts); s->incid = nullptr; s->release(s->masks);
   cudaStreamSynchronize(s->stream);
   for (auto& e : s->ev)
     if (e) cudaEventDestroy(e);
+  recycle_pinned(s->pin);
+  recycle_pinned_out(s->pin_out, s->pin_out_cap);
   delete s;
 }
 
@@ -560,6 +676,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   s->frame = F;
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, o.device);
   for (auto& e : s->ev) cudaEventCreate(&e);
+  s->pin = acquire_pinned();
+  if (!s->pin) {
+    delete s;
+    return fail(LOBE_E_CUDA, "pinned staging allocation failed");
+  }
   lobe_status rs = [&]() -> lobe_status {
     cudaStream_t st = s->stream;
     const int64_t G = g->n;
@@ -764,8 +885,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[10], st));
-    unsigned long long vc[2] = {0, 0};
-    CK(cudaMemcpyAsync(vc, s->vcnt, sizeof(vc), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(s->pin->vc, s->vcnt, sizeof(s->pin->vc), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(s->ev[2], st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
@@ -788,7 +908,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     if (s->N_loc > 0 && np > 0)
       KL(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
     // ---- a4 depth statistic over the non-empty (tile, camera) pairs
-    CK(cudaEventRecord(s->ev[4], st));
+    CK(cudaEventRecord(s->ev[11], st));
     CK(s->alloc(&s->pair_part, (size_t)std::max<int64_t>(np, 1)));
     CK(s->alloc(&s->cam_off, (size_t)NL + 1));
     CK(s->alloc(&s->cam_order, (size_t)std::max<int64_t>(np, 1)));
@@ -824,7 +944,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       }
       KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
     }
-    CK(cudaEventRecord(s->ev[5], st));
+    CK(cudaEventRecord(s->ev[12], st));
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
     CK(s->alloc(&s->word_zone, (size_t)s->words));
@@ -835,18 +955,16 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->ncb, (size_t)NL * kMaxBlocks));
     CK(s->alloc(&s->n0cb, (size_t)NL * kMaxBlocks));
     CK(s->alloc(&s->member, NL)); CK(s->alloc(&s->sel, NL)); CK(s->alloc(&s->home, NL));
-    CK(s->alloc(&s->counts, 3 * kMaxBlocks));
-    CK(s->alloc(&s->incid, kMaxBlocks));
+    {  // counts [3 x kMaxBlocks] u32 followed by incid [kMaxBlocks] u64 (one block, one copy)
+      static_assert((3 * kMaxBlocks * sizeof(uint32_t)) % 8 == 0, "incid alignment");
+      CK(s->alloc(&s->counts, 3 * kMaxBlocks + 2 * kMaxBlocks));
+      s->incid = reinterpret_cast<unsigned long long*>(s->counts + 3 * kMaxBlocks);
+    }
     CK(cudaEventRecord(s->ev[3], st));
-    CK(cudaStreamSynchronize(st));
-    s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
-    // visibility pass = culling kernel + test kernel (list building excluded)
-    s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
-    s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
-    s->st.t_depth_ms = ms_between(s->ev[4], s->ev[5]);
-    s->st.kept_tests = (uint64_t)kept_pairs * (uint64_t)kTile;  // pairs surviving the tile bound
-    s->st.dense_tests = (uint64_t)vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
-    s->st.accepted_tests = (uint64_t)vc[1] * (uint64_t)(kTile / 4);
+    // no synchronisation here: the depth statistic may still run while the caller
+    // enqueues the next call; event timings are read lazily (finalize_load_stats)
+    s->kept_pairs_last = kept_pairs;
+    s->stats_pending = true;
     s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
     s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
     s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
@@ -878,18 +996,25 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
   TRY(check_grid(grid, &g));
   TRY(ensure_eval(s, g));
   const size_t NL = (size_t)s->N_loc;
-  TRY(copy_out(s, K, s->K, NL * 4));
-  TRY(copy_out(s, depth_mean, s->D, NL * 8));
-  TRY(copy_out(s, z_min, s->zmin, NL * 4));
-  TRY(copy_out(s, z_max, s->zmax, NL * 4));
-  if (n_cb || n0_cb) {
-    // device layout is [c][B] with B = g.B stride
-    TRY(copy_out(s, n_cb, s->ncb, NL * g.B * 4));
-    TRY(copy_out(s, n0_cb, s->n0cb, NL * g.B * 4));
-  }
-  TRY(copy_out(s, member, s->member, NL * 8));
-  TRY(copy_out(s, home, s->home, NL * 4));
-  CK(cudaStreamSynchronize(s->stream));
+  std::vector<StagedCopy> plan;
+  std::vector<const void*> srcs;
+  size_t used = 0;
+  auto add = [&](void* dst, const void* src, size_t bytes) -> lobe_status {
+    const size_t before = plan.size();
+    TRY(stage_out(s, plan, used, dst, src, bytes));
+    if (plan.size() != before) srcs.push_back(src);
+    return LOBE_OK;
+  };
+  TRY(add(K, s->K, NL * 4));
+  TRY(add(depth_mean, s->D, NL * 8));
+  TRY(add(z_min, s->zmin, NL * 4));
+  TRY(add(z_max, s->zmax, NL * 4));
+  // device layout of n, n0 is [c][B] with B = g.B stride
+  TRY(add(n_cb, s->ncb, NL * g.B * 4));
+  TRY(add(n0_cb, s->n0cb, NL * g.B * 4));
+  TRY(add(member, s->member, NL * 8));
+  TRY(add(home, s->home, NL * 4));
+  TRY(run_staged(s, plan, used, srcs));
   return LOBE_OK;
 }
 
@@ -902,8 +1027,8 @@ lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_lo
   TRY(check_grid(grid, &g));
   TRY(ensure_eval(s, g));
   uint64_t inc[kMaxBlocks];
-  for (int b = 0; b < g.B; ++b) inc[b] = s->h_incid[b];
-  fill_records(s, g, s->h_ncams, inc, s->h_gvis, out, objective);
+  for (int b = 0; b < g.B; ++b) inc[b] = s->h_incid()[b];
+  fill_records(s, g, s->h_ncams(), inc, s->h_gvis(), out, objective);
   return LOBE_OK;
 }
 
@@ -965,8 +1090,8 @@ lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d
   s->ev_valid = false;  // masks go to the caller's buffer; do not cache
   CK(cudaMemsetAsync(d_masks, 0, sizeof(uint32_t) * g.B * s->words, s->stream));
   TRY(evaluate(s, g, d_masks));
-  if (n_cams) CK(cudaMemcpy(n_cams, s->h_ncams, sizeof(uint32_t) * g.B, cudaMemcpyDefault));
-  if (incid) CK(cudaMemcpy(incid, s->h_incid, sizeof(uint64_t) * g.B, cudaMemcpyDefault));
+  if (n_cams) CK(cudaMemcpy(n_cams, s->h_ncams(), sizeof(uint32_t) * g.B, cudaMemcpyDefault));
+  if (incid) CK(cudaMemcpy(incid, s->h_incid(), sizeof(uint64_t) * g.B, cudaMemcpyDefault));
   return LOBE_OK;
 }
 
@@ -1052,8 +1177,19 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   return LOBE_OK;
 }
 
+lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* n_cameras, int64_t* n_local_cameras,
+                            int64_t* cam_begin) {
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (n_gaussians) *n_gaussians = s->st.n_gaussians;
+  if (n_cameras) *n_cameras = s->st.n_cameras;
+  if (n_local_cameras) *n_local_cameras = s->st.n_local_cameras;
+  if (cam_begin) *cam_begin = s->st.cam_begin;
+  return LOBE_OK;
+}
+
 lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
+  finalize_load_stats(const_cast<lobe_scene*>(s));
   *out = s->st;
   return LOBE_OK;
 }
@@ -1098,7 +1234,7 @@ lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lo
       return 1;
     }
     uint32_t b = 0;
-    for (int k = 0; k < g.B; ++k) b = std::max(b, s->h_gvis[k]);
+    for (int k = 0; k < g.B; ++k) b = std::max(b, s->h_gvis()[k]);
     *val = b;
     return 0;
   };

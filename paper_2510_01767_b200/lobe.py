@@ -23,7 +23,7 @@ FRAME_AUTO_CENTER, FRAME_AUTO_RADIUS, FRAME_AUTO_AXES, FRAME_AUTO_ALL = 1, 2, 4,
 EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign_cameras", "lobe_block_loads",
            "lobe_crop_masks", "lobe_balance_partition", "lobe_bo_run", "lobe_mask_words", "lobe_block_partial",
            "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
-           "lobe_get_stats", "lobe_version", "lobe_dev_vis_bench"]
+           "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench"]
 
 
 class LobeError(RuntimeError):
@@ -222,8 +222,9 @@ class Scene:
         self.handle = h
         self.frame = dict(center=np.array(fr.center[:], np.float32), radius=np.float32(fr.radius),
                           axis_u=np.array(fr.axis_u[:], np.float32), axis_v=np.array(fr.axis_v[:], np.float32))
-        s = self.stats()
-        self.G, self.N, self.n_local, self.cam_begin = s.n_gaussians, s.n_cameras, s.n_local_cameras, s.cam_begin
+        info = [ctypes.c_int64() for _ in range(4)]
+        _check(L.lobe_scene_info(h, *[ctypes.byref(x) for x in info]))  # does not wait for the device
+        self.G, self.N, self.n_local, self.cam_begin = [x.value for x in info]
 
     def close(self):
         if getattr(self, "handle", None):
@@ -343,16 +344,20 @@ class Scene:
         return c, e
 
 
+_BLOCKLOAD_DT = None
+
+
 def records_to_dict(recs, objective):
+    global _BLOCKLOAD_DT
+    if _BLOCKLOAD_DT is None:  # numpy view of lobe_block_load (built once: the ctypes -> dtype path is slow)
+        _BLOCKLOAD_DT = np.ctypeslib.as_array((BlockLoad * 1)()).dtype
+    a = np.frombuffer(recs, dtype=_BLOCKLOAD_DT)  # structured view, no per-record loop
     B = len(recs)
-    out = dict(block_id=np.array([r.block_id for r in recs], np.int32),
-               n_cams=np.array([r.n_cams for r in recs], np.uint32),
-               g_blk=np.array([r.g_blk for r in recs], np.uint32),
-               g_vis=np.array([r.g_vis for r in recs], np.uint32),
-               incidences=np.array([r.incidences for r in recs], np.uint64),
-               area=np.array([r.area for r in recs], np.float64),
-               g_avgvis=np.array([r.g_avgvis for r in recs], np.float64),
-               lohi=np.array([[r.lo[0], r.lo[1], r.hi[0], r.hi[1]] for r in recs], np.float32).reshape(B, 4))
+    out = dict(block_id=a["block_id"].astype(np.int32), n_cams=a["n_cams"].astype(np.uint32),
+               g_blk=a["g_blk"].astype(np.uint32), g_vis=a["g_vis"].astype(np.uint32),
+               incidences=a["incidences"].astype(np.uint64), area=a["area"].astype(np.float64),
+               g_avgvis=a["g_avgvis"].astype(np.float64),
+               lohi=np.concatenate([a["lo"], a["hi"]], axis=1).astype(np.float32).reshape(B, 4))
     out["objective"] = objective if objective is not None else int(out["g_vis"].max()) if B else 0
     return out
 
