@@ -1062,18 +1062,41 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   }
   const int64_t W64 = (s->G + 63) / 64;
   const size_t bytes = (size_t)g.B * W64 * 8;
-  uint32_t *dc = nullptr, *de = nullptr, *mt = nullptr;
-  if (crop) CK(s->alloc(&dc, bytes / 4));
-  if (eligible) CK(s->alloc(&de, bytes / 4));
-  CK(s->alloc(&mt, (size_t)g.B * s->words));
+  // device destinations are written in place; host ones through scratch + copy
+  auto on_device = [&](const void* p) {
+    cudaPointerAttributes at{};
+    const bool d = p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+                   at.device == s->device;
+    cudaGetLastError();
+    return d;
+  };
+  const bool crop_dev = on_device(crop), elig_dev = on_device(eligible);
+  uint32_t *dc = nullptr, *de = nullptr;
+  if (crop) {
+    if (crop_dev) dc = reinterpret_cast<uint32_t*>(crop);
+    else CK(s->alloc(&dc, bytes / 4));
+  }
+  if (eligible) {
+    if (elig_dev) de = reinterpret_cast<uint32_t*>(eligible);
+    else CK(s->alloc(&de, bytes / 4));
+  }
+  uint64_t* mbits = nullptr;
+  uint8_t* cb8 = nullptr;
+  CK(s->alloc(&mbits, (size_t)s->words * 32));
+  CK(s->alloc(&cb8, (size_t)s->words * 32));
   CK(cudaEventRecord(s->ev[5], s->stream));
-  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mt, dc, de, s->stream));
+  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream));
   CK(cudaEventRecord(s->ev[6], s->stream));
-  TRY(copy_out(s, crop, dc, bytes));
-  TRY(copy_out(s, eligible, de, bytes));
-  s->release(dc);
-  s->release(de);
-  s->release(mt);
+  if (crop && !crop_dev) {
+    TRY(copy_out(s, crop, dc, bytes));
+    s->release(dc);
+  }
+  if (eligible && !elig_dev) {
+    TRY(copy_out(s, eligible, de, bytes));
+    s->release(de);
+  }
+  s->release(mbits);
+  s->release(cb8);
   CK(cudaStreamSynchronize(s->stream));
   s->st.t_crop_ms = ms_between(s->ev[5], s->ev[6]);
   return LOBE_OK;
