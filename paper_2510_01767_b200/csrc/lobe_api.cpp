@@ -99,7 +99,8 @@ struct lobe_scene {
   CamSetup* cams = nullptr;
   float *d_cam_gu = nullptr, *d_cam_gv = nullptr;
   uint32_t* rows = nullptr;
-  uint8_t* flags = nullptr;
+  uint8_t* flags = nullptr;     // dev bench (camera-inner variants) only
+  uint8_t* nonempty = nullptr;  // [kept pairs] any Gaussian visible
   PairPartial* pair_part = nullptr;
   uint32_t* cam_off = nullptr;
   int32_t* cam_order = nullptr;
@@ -622,7 +623,7 @@ void lobe_free_scene(lobe_scene* s) {
   cudaSetDevice(s->device);
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
-  s->release(s->rows); s->release(s->flags); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
+  s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
   s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
@@ -812,8 +813,6 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     // ---- a3/a4 visibility pass
     CK(s->alloc(&s->rows, (size_t)NL * s->words));
-    CK(s->alloc(&s->flags, (size_t)s->n_tiles * NL));
-    CK(cudaMemsetAsync(s->flags, 0, (size_t)s->n_tiles * NL, st));
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
@@ -855,6 +854,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaStreamSynchronize(st));
     s->n_units = nu;
     CK(s->alloc(&s->klist, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
+    CK(s->alloc(&s->nonempty, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
+    CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
     CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
     CK(s->alloc(&s->queue, 1));
     if (s->N_loc > 0 && kept_pairs > 0) {
@@ -875,7 +876,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.n_chunks = s->n_chunks;
       va.words = s->words;
       va.rows = s->rows;
-      va.flags = s->flags;
+      va.flags = nullptr;
+      va.nonempty = s->nonempty;
       va.keep = s->keep;
       va.n_sub = s->n_sub;
       va.slo = s->slice_lo;
@@ -892,7 +894,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     uint32_t* cnt;
     CK(s->alloc(&cnt, (size_t)s->n_tiles + 1));
     CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
-    if (s->N_loc > 0) KL(launch_tile_count(s->flags, s->n_tiles, s->N_loc, cnt, st));
+    if (s->N_loc > 0 && kept_pairs > 0) KL(launch_tile_count(s->koff, s->nonempty, s->n_tiles, cnt, st));
     size_t sb = 0;
     CK(exclusive_scan_u32(nullptr, sb, cnt, s->tile_off, s->n_tiles + 1, st));
     CK(cudaMallocAsync(&tmp, sb, st));
@@ -906,7 +908,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->pair_cam, (size_t)np));
     CK(s->alloc(&s->pair_tile, (size_t)np));
     if (s->N_loc > 0 && np > 0)
-      KL(launch_tile_fill(s->flags, s->n_tiles, s->N_loc, s->tile_off, s->pair_cam, s->pair_tile, st));
+      KL(launch_tile_fill(s->koff, s->klist, s->nonempty, s->n_tiles, s->tile_off, s->pair_cam, s->pair_tile, st));
     // ---- a4 depth statistic over the non-empty (tile, camera) pairs
     CK(cudaEventRecord(s->ev[11], st));
     CK(s->alloc(&s->pair_part, (size_t)std::max<int64_t>(np, 1)));
@@ -1154,7 +1156,7 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
   const size_t W32 = (size_t)((s->G + 31) / 32);
   uint32_t* d = nullptr;
   CK(s->alloc(&d, W32 * count));
-  KL(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, s->flags, s->N_loc, d, s->stream));
+  KL(launch_export_rows(s->G, s->iperm, s->rows, s->words, c0, count, s->keep, s->n_sub, d, s->stream));
   TRY(copy_out(s, rows, d, W32 * count * 4));
   s->release(d);
   CK(cudaStreamSynchronize(s->stream));
@@ -1178,7 +1180,8 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.n_chunks = s->n_chunks;
   va.words = s->words;
   va.rows = s->rows;
-  va.flags = s->flags;
+  va.flags = nullptr;
+  va.nonempty = s->nonempty;
   va.keep = s->keep;
   va.n_sub = s->n_sub;
   va.slo = s->slice_lo;

@@ -78,7 +78,8 @@ struct VisArgs {
   int64_t n_chunks;
   int64_t words;       // row stride in u32 words (G_pad / 32)
   uint32_t* rows;
-  uint8_t* flags;      // [n_tiles x n_cams], zeroed before the pass; 1 = some Gaussian visible
+  uint8_t* flags;      // camera-inner variants only (may be NULL): [n_tiles x n_cams] any-visible flags
+  uint8_t* nonempty;   // k_vis_tiles: [kept pairs], zeroed before the pass; 1 = some Gaussian visible
   const uint32_t* keep;  // [n_tiles x n_sub] camera masks surviving tile culling (NULL: dense)
   int64_t n_sub;         // ceil(n_cams / 32)
   const float4* slo;     // [n_tiles x 4] slice boxes (256 Gaussians) for k_vis_tiles
@@ -116,13 +117,13 @@ cudaError_t launch_cam_counts(int64_t n_pairs, const uint32_t* pair_cam, uint32_
 cudaError_t launch_iota(int32_t* v, int64_t n, cudaStream_t st);
 cudaError_t launch_depth_reduce(int64_t n_cams, const uint32_t* cam_off, const int32_t* order, const PairPartial* part,
                                 uint32_t* K, double* D, float* zmin, float* zmax, cudaStream_t st);
-// tile -> camera lists (CSR) from flags.
-cudaError_t launch_tile_count(const uint8_t* flags, int64_t n_tiles, int64_t n_cams, uint32_t* counts,
+// tile -> camera lists (CSR) of the non-empty pairs, from the kept lists and nonempty bytes.
+cudaError_t launch_tile_count(const uint32_t* koff, const uint8_t* nonempty, int64_t n_tiles, uint32_t* counts,
                               cudaStream_t st);
 cudaError_t exclusive_scan_u32(void* tmp, size_t& tmp_bytes, const uint32_t* in, uint32_t* out, int64_t n,
                                cudaStream_t st);
-cudaError_t launch_tile_fill(const uint8_t* flags, int64_t n_tiles, int64_t n_cams, const uint32_t* offsets,
-                             uint32_t* pair_cam, uint32_t* pair_tile, cudaStream_t st);
+cudaError_t launch_tile_fill(const uint32_t* koff, const uint32_t* klist, const uint8_t* nonempty, int64_t n_tiles,
+                             const uint32_t* offsets, uint32_t* pair_cam, uint32_t* pair_tile, cudaStream_t st);
 
 // a5: per-Gaussian zone pair, per-word / per-tile uniform zone, per-zone counts.
 cudaError_t launch_zones(const ZoneTables* dz, int nzv, int nzp, int64_t G, int64_t G_pad, const float* gu,
@@ -166,7 +167,7 @@ cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, con
                         const uint32_t* masks, int64_t words, int B, uint64_t* mbits, uint8_t* cb8, uint32_t* crop32,
                         uint32_t* elig32, cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
-                               int64_t count, const uint8_t* flags, int64_t n_cams, uint32_t* out, cudaStream_t st);
+                               int64_t count, const uint32_t* keep, int64_t n_sub, uint32_t* out, cudaStream_t st);
 // G_blk from per-zone-pair counts.
 cudaError_t launch_gblk(const ZoneTables* dz, int nzv, int nzp, const uint32_t* zp_count, uint32_t* gblk,
                         cudaStream_t st);
