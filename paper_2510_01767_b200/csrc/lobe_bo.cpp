@@ -23,6 +23,7 @@
 #include <map>
 #include <string>
 #include <vector>
+#include <thread>
 
 namespace lobe {
 namespace {
@@ -104,12 +105,29 @@ struct GP {
     const double r = std::sqrt(5.0 * r2);
     return sf2 * (1.0 + r + r * r / 3.0) * std::exp(-r);  // Matern-5/2
   }
+  std::vector<double> dX;  // X_i - X_j per dimension, j <= i (packed), filled once per data set
+  double kern_ij(int i, int j) const {  // == kern(X_i, X_j), same operations on the cached differences
+    const double* dd = &dX[((size_t)i * (i + 1) / 2 + j) * D];
+    double r2 = 0;
+    for (int d = 0; d < D; ++d) {
+      const double t = dd[d] / ls[d];
+      r2 += t * t;
+    }
+    const double r = std::sqrt(5.0 * r2);
+    return sf2 * (1.0 + r + r * r / 3.0) * std::exp(-r);
+  }
   // Cholesky of K + noise I; returns false if not PD
   bool factor(double nz) {
+    if (dX.size() != (size_t)n * (n + 1) / 2 * D) {
+      dX.resize((size_t)n * (n + 1) / 2 * D);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j)
+          for (int d = 0; d < D; ++d) dX[((size_t)i * (i + 1) / 2 + j) * D + d] = X[(size_t)i * D + d] - X[(size_t)j * D + d];
+    }
     Lc.assign((size_t)n * n, 0.0);
     for (int i = 0; i < n; ++i)
       for (int j = 0; j <= i; ++j) {
-        double s = kern(&X[(size_t)i * D], &X[(size_t)j * D]) + (i == j ? nz : 0.0);
+        double s = kern_ij(i, j) + (i == j ? nz : 0.0);
         for (int k = 0; k < j; ++k) s -= Lc[(size_t)i * n + k] * Lc[(size_t)j * n + k];
         if (i == j) {
           if (!(s > 0)) return false;
@@ -157,47 +175,55 @@ struct GP {
     }
     return -0.5 * q - ld;
   }
-  void fit() {
-    // multi-start coordinate search over log length scales and log signal variance
-    const double starts[3] = {0.2, 0.5, 1.0};
-    double best = -1e301;
-    std::vector<double> best_ls(D, 0.5);
-    double best_sf = 1.0;
-    for (double s0 : starts) {
-      ls.assign(D, s0);
-      sf2 = 1.0;
-      noise = 1e-6;
-      double cur = lml();
-      double step = 2.0;
-      for (int sweep = 0; sweep < 4; ++sweep) {
-        bool improved = false;
-        for (int d = 0; d <= D; ++d) {
-          for (double f : {step, 1.0 / step}) {
-            double* p = (d < D) ? &ls[d] : &sf2;
-            const double old = *p;
-            const double nv = std::min(std::max(old * f, d < D ? 0.01 : 0.05), d < D ? 10.0 : 20.0);
-            if (nv == old) continue;
-            *p = nv;
-            noise = 1e-6;
-            const double v = lml();
-            if (v > cur + 1e-12) {
-              cur = v;
-              improved = true;
-            } else {
-              *p = old;
-            }
+  // one start of the coordinate search (ascent on the log marginal likelihood)
+  double fit_from(double s0) {
+    ls.assign(D, s0);
+    sf2 = 1.0;
+    noise = 1e-6;
+    double cur = lml();
+    double step = 2.0;
+    for (int sweep = 0; sweep < 4; ++sweep) {
+      bool improved = false;
+      for (int d = 0; d <= D; ++d) {
+        for (double f : {step, 1.0 / step}) {
+          double* p = (d < D) ? &ls[d] : &sf2;
+          const double old = *p;
+          const double nv = std::min(std::max(old * f, d < D ? 0.01 : 0.05), d < D ? 10.0 : 20.0);
+          if (nv == old) continue;
+          *p = nv;
+          noise = 1e-6;
+          const double v = lml();
+          if (v > cur + 1e-12) {
+            cur = v;
+            improved = true;
+          } else {
+            *p = old;
           }
         }
-        if (!improved) step = std::sqrt(step);
       }
-      if (cur > best) {
-        best = cur;
-        best_ls = ls;
-        best_sf = sf2;
-      }
+      if (!improved) step = std::sqrt(step);
     }
-    ls = best_ls;
-    sf2 = best_sf;
+    return cur;
+  }
+  void fit() {
+    // multi-start coordinate search over log length scales and log signal variance;
+    // the starts run on their own threads (independent copies), the winner is
+    // chosen in start order exactly as a sequential loop would
+    const double starts[3] = {0.2, 0.5, 1.0};
+    GP runs[3] = {*this, *this, *this};
+    double vals[3];
+    std::thread th[3];
+    for (int k = 0; k < 3; ++k) th[k] = std::thread([&, k] { vals[k] = runs[k].fit_from(starts[k]); });
+    for (auto& t : th) t.join();
+    double best = -1e301;
+    int bk = 0;
+    for (int k = 0; k < 3; ++k)
+      if (vals[k] > best) {
+        best = vals[k];
+        bk = k;
+      }
+    ls = runs[bk].ls;
+    sf2 = runs[bk].sf2;
     noise = 1e-6;
     refactor();
   }
@@ -316,15 +342,28 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
     Rng rng(seed * 0x9E3779B97F4A7C15ull + (uint64_t)l);
     std::vector<double> bx(D), cand(D);
     double bei = -1.0;
-    for (int k = 0; k < 1024; ++k) {
-      for (int d = 0; d < D; ++d) cand[d] = rng.uniform();
-      double mu, s;
-      gp.predict(cand.data(), &mu, &s);
-      const double e = ei(mu, s, best_s);
-      if (e > bei) {
-        bei = e;
-        bx = cand;
-      }
+    {
+      // candidates drawn in sequence, scored on threads; the first maximum in
+      // candidate order wins, exactly as a sequential scan
+      constexpr int kCand = 1024, kThreads = 8;
+      std::vector<double> C((size_t)kCand * D), E(kCand);
+      for (int k = 0; k < kCand; ++k)
+        for (int d = 0; d < D; ++d) C[(size_t)k * D + d] = rng.uniform();
+      std::thread th[kThreads];
+      for (int q = 0; q < kThreads; ++q)
+        th[q] = std::thread([&, q] {
+          for (int k = q; k < kCand; k += kThreads) {
+            double mu, s;
+            gp.predict(&C[(size_t)k * D], &mu, &s);
+            E[k] = ei(mu, s, best_s);
+          }
+        });
+      for (auto& t : th) t.join();
+      for (int k = 0; k < kCand; ++k)
+        if (E[k] > bei) {
+          bei = E[k];
+          bx.assign(C.begin() + (size_t)k * D, C.begin() + (size_t)(k + 1) * D);
+        }
     }
     double step = 0.1;
     for (int it = 0; it < 20; ++it) {
