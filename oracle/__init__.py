@@ -166,6 +166,43 @@ def visibility(scene, pre, cams=None, threads=None):
     return dict(rows=rows, K=K, S=S, Om=Om, D=D, zmin=zmin, zmax=zmax)
 
 
+PRED_ISO, PRED_ANISO = 0, 1
+
+
+def cov(scene):
+    """O6a per-Gaussian 3D covariance {S00, S01, S02, S11, S12, S22} (ledger L24)."""
+    L = lib()
+    out = np.empty((scene.G, 6), np.float32)
+    _chk(L.oracle_cov(ctypes.c_int64(scene.G), _p(scene.sx), _p(scene.sy), _p(scene.sz), _p(scene.qw),
+                      _p(scene.qx), _p(scene.qy), _p(scene.qz), _p(out)), "cov")
+    return out
+
+
+def visibility_aniso(scene, pre, cams=None, threads=None):
+    """O6a/O7 with the projected-covariance footprint (ledger L24)."""
+    L = lib()
+    G = scene.G
+    sel = None if cams is None else np.ascontiguousarray(cams, np.int64)
+    ns = scene.N if sel is None else int(sel.shape[0])
+    words = (G + 31) // 32
+    rows = np.empty((ns, words), np.uint32)
+    K = np.empty(ns, np.uint32)
+    S = np.empty(ns, np.float64)
+    Om = np.empty(ns, np.float64)
+    zmin = np.empty(ns, np.float32)
+    zmax = np.empty(ns, np.float32)
+    cv = pre.get("cov")
+    if cv is None:
+        cv = pre["cov"] = cov(scene)
+    _chk(L.oracle_visibility_aniso(ctypes.c_int64(G), _p(scene.x), _p(scene.y), _p(scene.z), _p(cv),
+                                   _p(pre["gate"]), _p(scene.opacity), ctypes.c_int64(ns), _p(sel), _cams(scene),
+                                   _p(rows), _p(K), _p(S), _p(Om), _p(zmin), _p(zmax),
+                                   ctypes.c_int(threads or nthreads())), "visibility_aniso")
+    with np.errstate(invalid="ignore", divide="ignore"):
+        D = np.where(K > 0, S / np.where(Om > 0, Om, 1.0), 0.0)   # O7
+    return dict(rows=rows, K=K, S=S, Om=Om, D=D, zmin=zmin, zmax=zmax)
+
+
 def default_grid(m, n, v=None, h=None, delta_v=None, delta_h=None, tau=None):
     """Uniform cuts (v0_i = i/m) and the paper's defaults
     delta = (0.1/m, 0.1/n) in fp32 (ledger L14), tau = 0.15."""
@@ -232,16 +269,20 @@ def crop(scene, pre, grid, M):
     return c, e
 
 
-def run(scene, grid=None, mode=MODE_RATIO, frame_args=None, threads=None, masks=True):
+def run(scene, grid=None, mode=MODE_RATIO, frame_args=None, threads=None, masks=True, predicate=PRED_ISO):
     """The whole path in the paper's order: validate, frame, per-Gaussian /
-    per-camera setup, visibility, assignment, block loads, crop."""
+    per-camera setup, visibility (isotropic O6 or anisotropic O6a), assignment,
+    block loads, crop."""
     validate(scene)
     cfg = scene.cfg
     if grid is None:
         grid = default_grid(cfg.m, cfg.n)
     fr = frame(scene, **(frame_args or {}))
     pre = prep(scene, fr)
-    vis = visibility(scene, pre, threads=threads)
+    if predicate == PRED_ANISO:
+        vis = visibility_aniso(scene, pre, threads=threads)
+    else:
+        vis = visibility(scene, pre, threads=threads)
     asg = assign(scene, pre, vis, grid, threads=threads)
     bl = block_loads(scene, pre, vis, asg, grid, mode=mode, masks=masks)
     out = dict(frame=fr, pre=pre, vis=vis, asg=asg, loads=bl, grid=grid)

@@ -375,6 +375,126 @@ int oracle_visibility(int64_t G, const float* x, const float* y, const float* z,
   return O_OK;
 }
 
+// ------------------------------------------------ O6a anisotropic predicate
+// SURVEY §8f NEXT-2 / ledger L24: the projected-covariance footprint of SPEC.md
+// :338 and :387 (EWA: Sigma' = J W Sigma W^T J^T + 0.3 I, radius 3 sqrt(lambda_max),
+// S:299's "3 sigma footprint from projected covariance") replaces the isotropic
+// bound; depth range and opacity gate as in O6.
+//
+// Per Gaussian (oracle_cov): rotation from the quaternion as given (validated
+// unit norm, not renormalised), M = R diag(s), Sigma = M M^T:
+//   r00 = 1 - 2(y y + z z), r01 = 2(x y - w z), r02 = 2(x z + w y),
+//   r10 = 2(x y + w z), r11 = 1 - 2(x x + z z), r12 = 2(y z - w x),
+//   r20 = 2(x z - w y), r21 = 2(y z + w x), r22 = 1 - 2(x x + y y),
+//   M_ij = r_ij s_j, Sigma_ij = fma(M_i0, M_j0, fma(M_i1, M_j1, M_i2 M_j2)).
+// cov: 6 floats per Gaussian {S00, S01, S02, S11, S12, S22}; trace out (for the
+// GPU's culling bound it is not needed here).
+int oracle_cov(int64_t G, const float* sx, const float* sy, const float* sz, const float* qw, const float* qx,
+               const float* qy, const float* qz, float* cov) {
+  for (int64_t i = 0; i < G; ++i) {
+    const float w = qw[i], x = qx[i], y = qy[i], z = qz[i];
+    float r[9];
+    r[0] = 1.0f - 2.0f * (y * y + z * z);
+    r[1] = 2.0f * (x * y - w * z);
+    r[2] = 2.0f * (x * z + w * y);
+    r[3] = 2.0f * (x * y + w * z);
+    r[4] = 1.0f - 2.0f * (x * x + z * z);
+    r[5] = 2.0f * (y * z - w * x);
+    r[6] = 2.0f * (x * z - w * y);
+    r[7] = 2.0f * (y * z + w * x);
+    r[8] = 1.0f - 2.0f * (x * x + y * y);
+    const float s[3] = {sx[i], sy[i], sz[i]};
+    float M[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) M[3 * a + b] = r[3 * a + b] * s[b];
+    auto sig = [&](int a, int b) {
+      return std::fmaf(M[3 * a], M[3 * b], std::fmaf(M[3 * a + 1], M[3 * b + 1], M[3 * a + 2] * M[3 * b + 2]));
+    };
+    float* c = cov + 6 * i;
+    c[0] = sig(0, 0); c[1] = sig(0, 1); c[2] = sig(0, 2);
+    c[3] = sig(1, 1); c[4] = sig(1, 2); c[5] = sig(2, 2);
+  }
+  return O_OK;
+}
+
+// Per (camera c, Gaussian i), with the camera's raw fp32 R (rows), t, fx, fy,
+// cx, cy, W, H, z_near, z_far (no pre-scaling):
+//   xc = fma(R00, x, fma(R01, y, fma(R02, z, t0)))      (yc, zc: rows 1, 2)
+//   depth ok: zc > zn && zc < zf      (invisible otherwise; nothing else evaluated)
+//   iz = 1 / zc;  a = xc iz;  b = yc iz;  upix = fma(fx, a, cx);  vpix = fma(fy, b, cy)
+//   j00 = fx iz;  j11 = fy iz;  j02 = -(j00 a);  j12 = -(j11 b)
+//   T0k = fma(j00, R0k, j02 R2k);  T1k = fma(j11, R1k, j12 R2k)          (T = J W)
+//   V0i = fma(Si0, T00, fma(Si1, T01, Si2 T02)), V1i likewise with T1   (V = Sigma T^T)
+//   A = fma(T00, V00, fma(T01, V01, T02 V02)) + 0.3
+//   B = fma(T10, V00, fma(T11, V01, T12 V02))
+//   C = fma(T10, V10, fma(T11, V11, T12 V12)) + 0.3
+//   mid = 0.5 (A + C);  d = 0.5 (A - C);  disc = fma(d, d, B B)
+//   r = 3 sqrt(mid + sqrt(disc))
+//   visible = gate && depth ok && upix >= -r && upix <= W + r && vpix >= -r && vpix <= H + r
+// (all IEEE binary32, round to nearest; division and square roots correctly
+// rounded). The depth statistic uses w = zc (the same fma chain as O6's w).
+int oracle_visibility_aniso(int64_t G, const float* x, const float* y, const float* z, const float* cov,
+                            const uint8_t* gate, const float* o, int64_t nsel, const int64_t* sel, const Cam* cams,
+                            uint32_t* rows, uint32_t* K, double* S, double* Om, float* zmin, float* zmax,
+                            int nthreads) {
+  const int64_t words = (G + 31) / 32;
+  parallel_for(nsel, nthreads, [&](int64_t j) {
+    const int64_t c = sel ? sel[j] : j;
+    const Cam& k = cams[c];
+    const float* R = k.R;
+    const float Wf = (float)k.width, Hf = (float)k.height;
+    uint32_t* row = rows + j * words;
+    std::fill(row, row + words, 0u);
+    uint32_t cnt = 0;
+    double sum_ow = 0.0, sum_o = 0.0;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int64_t i = 0; i < G; ++i) {
+      const float xc = std::fmaf(R[0], x[i], std::fmaf(R[1], y[i], std::fmaf(R[2], z[i], k.t[0])));
+      const float yc = std::fmaf(R[3], x[i], std::fmaf(R[4], y[i], std::fmaf(R[5], z[i], k.t[1])));
+      const float zc = std::fmaf(R[6], x[i], std::fmaf(R[7], y[i], std::fmaf(R[8], z[i], k.t[2])));
+      if (!gate[i] || !(zc > k.z_near && zc < k.z_far)) continue;
+      const float iz = 1.0f / zc;
+      const float a = xc * iz, b = yc * iz;
+      const float upix = std::fmaf(k.fx, a, k.cx), vpix = std::fmaf(k.fy, b, k.cy);
+      const float j00 = k.fx * iz, j11 = k.fy * iz;
+      const float j02 = -(j00 * a), j12 = -(j11 * b);
+      float T0[3], T1[3];
+      for (int q = 0; q < 3; ++q) {
+        T0[q] = std::fmaf(j00, R[q], j02 * R[6 + q]);
+        T1[q] = std::fmaf(j11, R[3 + q], j12 * R[6 + q]);
+      }
+      const float* cv = cov + 6 * i;
+      const float Sg[3][3] = {{cv[0], cv[1], cv[2]}, {cv[1], cv[3], cv[4]}, {cv[2], cv[4], cv[5]}};
+      float V0[3], V1[3];
+      for (int q = 0; q < 3; ++q) {
+        V0[q] = std::fmaf(Sg[q][0], T0[0], std::fmaf(Sg[q][1], T0[1], Sg[q][2] * T0[2]));
+        V1[q] = std::fmaf(Sg[q][0], T1[0], std::fmaf(Sg[q][1], T1[1], Sg[q][2] * T1[2]));
+      }
+      const float A = std::fmaf(T0[0], V0[0], std::fmaf(T0[1], V0[1], T0[2] * V0[2])) + 0.3f;
+      const float B = std::fmaf(T1[0], V0[0], std::fmaf(T1[1], V0[1], T1[2] * V0[2]));
+      const float C = std::fmaf(T1[0], V1[0], std::fmaf(T1[1], V1[1], T1[2] * V1[2])) + 0.3f;
+      const float mid = 0.5f * (A + C), d = 0.5f * (A - C);
+      const float disc = std::fmaf(d, d, B * B);
+      const float r = 3.0f * std::sqrt(mid + std::sqrt(disc));
+      const bool visible = upix >= -r && upix <= Wf + r && vpix >= -r && vpix <= Hf + r;
+      if (visible) {
+        row[i >> 5] |= 1u << (i & 31);
+        cnt += 1;
+        sum_ow += (double)o[i] * (double)zc;
+        sum_o += (double)o[i];
+        mn = std::min(mn, zc);
+        mx = std::max(mx, zc);
+      }
+    }
+    K[j] = cnt;
+    S[j] = sum_ow;
+    Om[j] = sum_o;
+    zmin[j] = mn;
+    zmax[j] = mx;
+  });
+  return O_OK;
+}
+
 // ------------------------------------------------------------- O8 assignment
 // n[c][b] = |{i in V_c : (gu_i, gv_i) in B^(b)}| over the enlarged regions
 // (PAPER.md:167, :176-178); n0 over the delta=0 cells. member bit b set iff
