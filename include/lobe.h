@@ -112,8 +112,17 @@ typedef struct {
   int32_t rank, world;  /* camera shard; world >= 1 */
   void* stream;         /* cudaStream_t; NULL = legacy default stream */
   int32_t assign_mode;  /* LOBE_ASSIGN_* */
-  int32_t reserved;
+  int32_t predicate;    /* LOBE_PREDICATE_* (0 = isotropic, the default) */
 } lobe_options;
+
+/* Visibility predicate. ISOTROPIC: SPEC.md:299's culling bound, footprint radius
+ * 3 max(s) max(fx, fy) / z (the measured path). ANISOTROPIC: the
+ * projected-covariance footprint of SPEC.md:338/:387 (EWA: Sigma' = J W Sigma
+ * W^T J^T + 0.3 I, radius 3 sqrt(lambda_max(Sigma')), Sigma from the rotation
+ * and scales, DESIGN.md ledger L24 pins the fp32 op order).
+ * Everything downstream (depth statistic, assignment, loads, crop) is shared. */
+#define LOBE_PREDICATE_ISOTROPIC 0
+#define LOBE_PREDICATE_ANISOTROPIC 1
 
 /* Grid cuts (GridCuts SPEC.md:51-56). v: m-1 cuts on the first
  * ground axis, h: n-1 cuts on the second, strictly increasing in (0,1).

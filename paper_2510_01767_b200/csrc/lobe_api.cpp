@@ -106,6 +106,9 @@ struct lobe_scene {
   int32_t* cam_order = nullptr;
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
   float4 *slice_lo = nullptr, *slice_hi = nullptr;
+  bool aniso = false;            // anisotropic predicate (ledger L24)
+  float4* cv = nullptr;          // pair-interleaved Sigma (anisotropic)
+  AnisoCam* acams = nullptr;     // per local camera (anisotropic)
   unsigned long long* vcnt = nullptr;  // k_vis_tiles counters: undecided, accepted
   uint32_t* keep = nullptr;
   unsigned long long* kept = nullptr;
@@ -265,6 +268,29 @@ CamSetup camera_setup(const lobe_camera& k) {
   s.zn = k.z_near;
   s.zf = k.z_far;
   return s;
+}
+
+// Anisotropic predicate: the raw camera, plus w2 >= ||R||_2^2 = max abs row sum
+// of R^T R (fp64) for the culling bound (ledger L24).
+AnisoCam aniso_setup(const lobe_camera& k) {
+  AnisoCam a{};
+  for (int i = 0; i < 9; ++i) a.R[i] = k.R[i];
+  for (int i = 0; i < 3; ++i) a.t[i] = k.t[i];
+  a.fx = k.fx; a.fy = k.fy; a.cx = k.cx; a.cy = k.cy;
+  a.Wf = (float)k.width; a.Hf = (float)k.height;
+  a.zn = k.z_near; a.zf = k.z_far;
+  double w2 = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    double row = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      double g = 0.0;
+      for (int r = 0; r < 3; ++r) g += (double)k.R[3 * r + i] * (double)k.R[3 * r + j];
+      row += std::fabs(g);
+    }
+    w2 = std::max(w2, row);
+  }
+  a.w2 = w2 * (1.0 + 1e-12);
+  return a;
 }
 
 // O3's fp32 map for one point (contraction + ground projection), host side.
@@ -624,7 +650,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -652,6 +678,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   if (opt) o = *opt;
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(LOBE_E_INVALID_CONFIG, "bad rank/world");
   if (o.assign_mode < 0 || o.assign_mode > 2) return fail(LOBE_E_INVALID_CONFIG, "bad assign_mode");
+  if (o.predicate != LOBE_PREDICATE_ISOTROPIC && o.predicate != LOBE_PREDICATE_ANISOTROPIC)
+    return fail(LOBE_E_INVALID_CONFIG, "bad predicate");
   TRY(validate_cameras(cams, n_cams));
   lobe_frame F{};
   if (inout_frame) F = *inout_frame;
@@ -674,6 +702,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   s->rank = o.rank;
   s->world = o.world;
   s->assign_mode = o.assign_mode;
+  s->aniso = (o.predicate == LOBE_PREDICATE_ANISOTROPIC);
   s->frame = F;
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, o.device);
   for (auto& e : s->ev) cudaEventCreate(&e);
@@ -718,6 +747,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     int32_t *vals, *perm;
     unsigned long long* err_idx;
     CK(s->alloc(&ru, G)); CK(s->alloc(&rv, G)); CK(s->alloc(&kk, G));
+    float* cov_raw = nullptr;  // anisotropic: Sigma per Gaussian, caller order
+    if (s->aniso) CK(s->alloc(&cov_raw, (size_t)6 * G));
     CK(s->alloc(&rec, (size_t)2 * G));
     CK(s->alloc(&keys, G)); CK(s->alloc(&keys_s, G)); CK(s->alloc(&vals, G)); CK(s->alloc(&perm, G));
     CK(s->alloc(&scratch, 8)); CK(s->alloc(&err_idx, 1));
@@ -735,6 +766,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       pin.av[a] = F.axis_v[a];
     }
     pin.rho = F.radius;
+    pin.cov = cov_raw;
     KL(launch_prep_raw(pin, ru, rv, kk, keys, vals, scratch, err_idx, scratch + 1, st));
     uint32_t hs[8];
     unsigned long long hbad;
@@ -767,7 +799,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->gu, (size_t)s->G_pad));
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
     CK(s->alloc(&s->iperm, (size_t)G));
-    KL(launch_pack(G, s->G_pad, perm, rec, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, st));
+    if (s->aniso) CK(s->alloc(&s->cv, (size_t)s->G_pad / 2 * 3));
+    KL(launch_pack(G, s->G_pad, perm, rec, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st));
+    s->release(cov_raw);
     cudaFreeAsync(tmp, st);
     s->release(ru); s->release(rv); s->release(kk); s->release(rec);
     s->release(keys); s->release(keys_s); s->release(vals); s->release(perm); s->release(scratch);
@@ -776,11 +810,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
 
     // ---- a2 camera setup (local shard) + camera-centre grid coords
     std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
+    std::vector<AnisoCam> haset(std::max<int64_t>(s->N_loc, 1));
     s->cam_gu.assign(s->N_loc, 0.f);
     s->cam_gv.assign(s->N_loc, 0.f);
     for (int64_t c = 0; c < s->N_loc; ++c) {
       const lobe_camera& k = cams[s->cam_begin + c];
       hset[c] = camera_setup(k);
+      if (s->aniso) haset[c] = aniso_setup(k);
       double oc[3];
       cam_centre(k, oc);
       float ru_, rv_;
@@ -795,6 +831,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->d_cam_gu, NL));
     CK(s->alloc(&s->d_cam_gv, NL));
     CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, st));
+    if (s->aniso) {
+      CK(s->alloc(&s->acams, NL));
+      CK(cudaMemcpyAsync(s->acams, haset.data(), sizeof(AnisoCam) * NL, cudaMemcpyHostToDevice, st));
+    }
     s->n_sub = (NL + 31) / 32;
     CK(s->alloc(&s->tile_lo, (size_t)s->n_tiles));
     CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
@@ -816,7 +856,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
-    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->N_loc, s->keep, s->kept, st));
+    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, st));
     CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
     unsigned long long kept_pairs = 0;
@@ -883,6 +923,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.slo = s->slice_lo;
       va.shi = s->slice_hi;
       va.counters = s->vcnt;
+      va.aniso = s->aniso;
+      va.cv = s->cv;
+      va.acams = s->acams;
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
@@ -1187,6 +1230,10 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.slo = s->slice_lo;
   va.shi = s->slice_hi;
   va.counters = nullptr;
+  va.aniso = s->aniso;
+  va.cv = s->cv;
+  va.acams = s->acams;
+  if (s->aniso && variant != 0) return fail(LOBE_E_INVALID_CONFIG, "camera-inner variants are isotropic only");
   int g = 0;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)

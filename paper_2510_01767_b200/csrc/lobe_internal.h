@@ -52,8 +52,21 @@ struct PrepIn {
   const float *x, *y, *z, *sx, *sy, *sz, *qw, *qx, *qy, *qz, *o;
   int64_t G;
   float c0[3], rho, au[3], av[3];
+  float* cov;  // anisotropic predicate: 6 floats per Gaussian (caller order), else NULL
 };
-// Validation + per-Gaussian raw ground coords and footprint radius. err[0] =
+
+// Anisotropic predicate (ledger L24): the raw camera parameters of the EWA
+// footprint test, plus w2 >= ||R||_2^2 (host: max absolute row sum of R^T R in
+// fp64) for the culling bound.
+struct __align__(16) AnisoCam {
+  float R[9], t[3];
+  float fx, fy, cx, cy;
+  float Wf, Hf, zn, zf;
+  double w2, pad;
+};
+static_assert(sizeof(AnisoCam) == 96, "AnisoCam layout");
+// Validation + per-Gaussian raw ground coords and footprint radius (isotropic:
+// k = 3 max(s); anisotropic: k = trace(Sigma) and Sigma into in.cov). err[0] =
 // error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
 // Also writes the 3D Morton sort key of the contracted centre and identity values.
 cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* keys, int32_t* vals,
@@ -64,9 +77,12 @@ cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const 
                              cudaStream_t st);
 cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                              int32_t* vout, int64_t n, cudaStream_t st);
-// Gather into the internal pair-interleaved layout, build the inverse permutation.
+// Gather into the internal pair-interleaved layout, build the inverse permutation;
+// anisotropic: also Sigma, cv[3 (32 g + l) + {0,1,2}] = {S00A,S00B,S01A,S01B},
+// {S02A,S02B,S11A,S11B}, {S12A,S12B,S22A,S22B}.
 cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float4* rec, float* xy, float* zk,
-                        float* o2, float* gu, float* gv, int32_t* iperm, cudaStream_t st);
+                        float* o2, float* gu, float* gv, int32_t* iperm, const float* cov_raw, float4* cv,
+                        cudaStream_t st);
 
 // a3: visibility tests -> rows, tile flags, per-(chunk,camera) partials.
 struct VisArgs {
@@ -85,6 +101,9 @@ struct VisArgs {
   const float4* slo;     // [n_tiles x 4] slice boxes (256 Gaussians) for k_vis_tiles
   const float4* shi;
   unsigned long long* counters;  // k_vis_tiles: [0] undecided, [1] accepted (slice, camera) pairs; may be NULL
+  int aniso;                     // 1: anisotropic predicate (ledger L24)
+  const float4* cv;              // anisotropic: pair-interleaved Sigma
+  const AnisoCam* acams;         // anisotropic: per local camera
 };
 
 // Tile culling: per camera the five linear forms of the
@@ -95,7 +114,7 @@ cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_til
                                float4* slo, float4* shi, cudaStream_t st);
 // hierarchical: chunk boxes (clo/chi scratch, n_tiles/16 each) then tile boxes
 cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float4* chi, int64_t n_tiles,
-                        const CamSetup* cams, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
+                        const CamSetup* cams, const AnisoCam* acams, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
                         cudaStream_t st);
 // kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,

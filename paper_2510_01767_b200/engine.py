@@ -50,12 +50,13 @@ class Engine:
         self._comb = None
 
     @classmethod
-    def from_scene(cls, gaussians, cameras, frame=None, device=None, stream=None, assign_mode=0, group=None):
+    def from_scene(cls, gaussians, cameras, frame=None, device=None, stream=None, assign_mode=0, group=None,
+                   predicate=0):
         from . import lobe
         rank, world = _world(group)
         dev = torch.cuda.current_device() if device is None else device
         sc = lobe.Scene(gaussians, cameras, frame=frame, device=dev, rank=rank, world=world, stream=stream,
-                        assign_mode=assign_mode)
+                        assign_mode=assign_mode, predicate=predicate)
         sc.device = f"cuda:{dev}"
         return cls(sc, group)
 

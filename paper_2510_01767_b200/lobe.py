@@ -26,6 +26,9 @@ EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign
            "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench"]
 
 
+PREDICATE_ISOTROPIC, PREDICATE_ANISOTROPIC = 0, 1  # lobe_options.predicate (DESIGN.md ledger L24)
+
+
 class LobeError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
@@ -53,7 +56,7 @@ class Frame(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("stream", ctypes.c_void_p), ("assign_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("stream", ctypes.c_void_p), ("assign_mode", ctypes.c_int32), ("predicate", ctypes.c_int32)]
 
 
 class Grid(ctypes.Structure):
@@ -180,7 +183,7 @@ class Scene:
     """Owning wrapper of a lobe_scene* handle."""
 
     def __init__(self, gaussians, cameras, frame=None, device=0, rank=0, world=1, stream=None,
-                 assign_mode=ASSIGN_RATIO):
+                 assign_mode=ASSIGN_RATIO, predicate=0):
         """gaussians: an object with x..opacity attributes (numpy host arrays or
         torch CUDA tensors); cameras: a synth Scene (its camera arrays) or a
         ctypes Camera array. frame: dict(center, radius, axis_u, axis_v) or None
@@ -215,7 +218,7 @@ class Scene:
             fr.axis_v[:] = [float(v) for v in frame["axis_v"]]
         fr.auto_flags = flags
         st = stream if (stream is None or isinstance(stream, int)) else stream.cuda_stream
-        opt = Options(int(device), int(rank), int(world), st, int(assign_mode), 0)
+        opt = Options(int(device), int(rank), int(world), st, int(assign_mode), int(predicate))
         h = ctypes.c_void_p()
         _check(L.lobe_load_scene(ctypes.byref(g), cams, len(cams), ctypes.byref(fr), ctypes.byref(opt),
                                  ctypes.byref(h)))

@@ -52,10 +52,10 @@ def _cmp_loads(L, o):
     assert L["objective"] == o["objective"]
 
 
-def full_parity(sc, grids, mode=0):
+def full_parity(sc, grids, mode=0, predicate=0):
     lobe = _lobe()
-    with lobe.Scene(sc, sc, assign_mode=mode) as S:
-        o0 = oracle.run(sc, grid=grids[0], mode=mode)
+    with lobe.Scene(sc, sc, assign_mode=mode, predicate=predicate) as S:
+        o0 = oracle.run(sc, grid=grids[0], mode=mode, predicate=predicate)
         c0, rho, au, av = o0["frame"]
         assert (S.frame["center"] == c0).all() and S.frame["radius"] == rho
         rows = S.export_rows()
@@ -415,3 +415,30 @@ def test_edge_clusters_exact(seed):
     sc = _edge_scene(seed)
     st = full_parity(sc, [oracle.default_grid(2, 2)])
     assert st.accepted_tests > 0 and st.dense_tests > 0 and st.kept_tests > st.dense_tests + st.accepted_tests
+
+
+# ---------------------------------------------------------------- anisotropic predicate (NEXT-2, ledger L24)
+def test_aniso_tiny_full(tiny_scene):
+    """The projected-covariance footprint path: rows, counts, depth statistics,
+    assignments, loads and masks equal the oracle's O6a (bit-exact; D_c 1e-6)."""
+    full_parity(tiny_scene, [oracle.default_grid(2, 2), _rand_grid(3, 3, 5)], predicate=1)
+
+
+def test_aniso_ragged():
+    from synth.scenes import make_config, make_scene
+    sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x2510AA01))
+    full_parity(sc, [oracle.default_grid(2, 2), _rand_grid(8, 8, 3)], predicate=1)
+
+
+@pytest.mark.parametrize("seed,G", [(1, 6000), (3, 50_000)])
+def test_aniso_fuzz_culling_exact(seed, G):
+    """Box bounds of the anisotropic mode (fp64, radius envelope from trace(Sigma)
+    and ||J||_F) never change a decision: cameras inside the cloud, heavy-tailed
+    scales and random rotations."""
+    full_parity(_fuzz_scene(seed, G=G), [oracle.default_grid(3, 2)], predicate=1)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_aniso_edge_clusters_exact(seed):
+    st = full_parity(_edge_scene(seed), [oracle.default_grid(2, 2)], predicate=1)
+    assert st.dense_tests > 0
