@@ -29,7 +29,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOP_PER_TEST = 22  # 9 FFMA (w,u,v) + 2 FFMA (edge tests), 2 flop each
+FLOP_PER_TEST_ISO = 22  # 9 FFMA (w,u,v) + 2 FFMA (edge tests), 2 flop each
+# anisotropic predicate (ledger L24): 9 FMA (xc,yc,zc) + 2 mul (a,b) + 2 FMA (upix,vpix) + 4 mul (J)
+# + 6 FMA + 6 mul (T) + 2 x 3 x (2 FMA + 1 mul) (V) + 3 x (2 FMA + 1 mul) + 2 add (A, B, C) + 2 add + 2 mul
+# (mid, d) + 1 FMA + 1 mul (disc) + 1 add + 1 mul (r) + 2 add (W + r, H + r) = 108 flop; the reciprocal and
+# the two square roots are not counted
+FLOP_PER_TEST_ANISO = 108
+FLOP_PER_TEST = FLOP_PER_TEST_ISO
 FP32_LANES_PER_SM = 128
 
 
@@ -44,6 +50,8 @@ def parse():
     p.add_argument("--no-bo", action="store_true")
     p.add_argument("--bo-L", type=int, default=100)
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--predicate", default="iso", choices=["iso", "aniso"],
+                   help="visibility predicate: iso = SPEC.md:299 bound (the metric's path), aniso = EWA footprint")
     return p.parse_args()
 
 
@@ -106,7 +114,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def cpu_baseline(sc, target_s=12.0):
+def cpu_baseline(sc, target_s=12.0, pred=0):
     """The oracle as it stands, on the host cores, on a bounded sample of the
     same workload: the visibility pass (O6/O7) and camera assignment (O8) of a
     random sample of cameras over all G Gaussians, all threads."""
@@ -117,6 +125,8 @@ def cpu_baseline(sc, target_s=12.0):
     oracle.validate(sc)
     fr = oracle.frame(sc)
     pre = oracle.prep(sc, fr)
+    if pred:
+        pre["cov"] = oracle.cov(sc)
     t_prep = time.perf_counter() - t0
     rng = np.random.default_rng(0)
     t_sample, done = 0.0, 0
@@ -125,12 +135,16 @@ def cpu_baseline(sc, target_s=12.0):
         sel = np.sort(rng.choice(sc.N, min(threads, sc.N), replace=False))
         pre["cam_gu_sel"], pre["cam_gv_sel"] = pre["cam_gu"][sel], pre["cam_gv"][sel]
         t1 = time.perf_counter()
-        vis = oracle.visibility(sc, pre, cams=sel, threads=threads)
+        if pred:
+            vis = oracle.visibility_aniso(sc, pre, cams=sel, threads=threads)
+        else:
+            vis = oracle.visibility(sc, pre, cams=sel, threads=threads)
         oracle.assign(sc, pre, vis, g, threads=threads)
         t_sample += time.perf_counter() - t1
         done += len(sel)
     return {"value": sc.G * done / t_sample, "unit": "tests/s", "cores": threads, "kind": "oracle",
-            "sample": f"{done} random cameras x all {sc.G} Gaussians: visibility (O6/O7) + assignment (O8), "
+            "sample": f"{done} random cameras x all {sc.G} Gaussians: visibility ({'O6a' if pred else 'O6'}/O7) "
+                      f"+ assignment (O8), "
                       f"{t_sample:.1f} s; per-Gaussian prep (O3, single thread) {t_prep:.1f} s not included",
             "cpu_seconds": t_sample + t_prep}
 
@@ -150,6 +164,8 @@ def run_reference(args, cfg_name):
     fr = oracle.frame(sc)
     t0 = time.perf_counter()
     pre = oracle.prep(sc, fr)
+    if pred:
+        pre["cov"] = oracle.cov(sc)
     t_prep = time.perf_counter() - t0
     rng = np.random.default_rng(1)
     per_step = max(1, threads)
@@ -199,6 +215,9 @@ def main():
     from paper_2510_01767_b200.engine import Engine
     from synth import make_scene, array_hashes
 
+    global FLOP_PER_TEST
+    pred = 1 if args.predicate == "aniso" else 0
+    FLOP_PER_TEST = FLOP_PER_TEST_ANISO if pred else FLOP_PER_TEST_ISO
     sc = make_scene(cfg_name)
     G, N, m, n = sc.G, sc.N, sc.cfg.m, sc.cfg.n
     B = m * n
@@ -220,7 +239,7 @@ def main():
                  "dense": 0, "pairs": 0, "kept": 0, "accepted": 0}
 
     def step(gsrc, crop_out, elig_out):
-        eng = Engine.from_scene(gsrc, cams, stream=stream, group=group)
+        eng = Engine.from_scene(gsrc, cams, stream=stream, group=group, predicate=pred)
         L = eng.block_loads(m, n)
         A = eng.assign_cameras(m, n)
         eng.crop_masks_into(m, n, crop_out, elig_out)
@@ -295,7 +314,7 @@ def main():
     # ---- BO loop (a10), reported separately
     bo = None
     if not args.no_bo:
-        eng = Engine.from_scene(dg, cams, stream=stream, group=group)
+        eng = Engine.from_scene(dg, cams, stream=stream, group=group, predicate=pred)
         barrier()
         t0 = time.perf_counter()
         r = eng.balance_partition(m, n, L=args.bo_L, seed=0)
@@ -333,15 +352,15 @@ def main():
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("config") == cfg_name and tj.get("world") == world:
+            if tj.get("config") == cfg_name and tj.get("world") == world and not pred:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
     clocks = clk.summary()
-    roof = {"bound": "alu", "kernel": "k_cull + k_vis_tiles (a3)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": "alu", "kernel": "k_cull + k_vis_tiles%s (a3)" % ("_aniso" if pred else ""), "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max_mhz:.0f} MHz "
-                          "(sm_max_mhz of MEASURED_PEAKS.json); 22 flop/test",
+                          "(sm_max_mhz of MEASURED_PEAKS.json); %d flop/test" % FLOP_PER_TEST,
             "kernel_ms": t_vis, "cull_ms": t_cull, "kernel_share_of_step": t_vis / ms,
             "executed_tests": int(dense_tests), "logical_tests": int(G * n_local),
             "executed_fraction": dense_tests / float(G * n_local),
@@ -359,12 +378,13 @@ def main():
             "frac_at_measured_clock": (achieved / (peak * (clocks["sm_mhz"] or sm_max_mhz) / sm_max_mhz))}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(sc)
+        cpu = cpu_baseline(sc, pred=pred)
     line = {"metric": "gaussian_camera_visibility_tests_per_s", "value": value, "unit": "tests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"{cfg_name}-shaped", "G": G, "N": N, "grid": f"{m}x{n}",
+                       "predicate": "anisotropic (EWA, ledger L24)" if pred else "isotropic (SPEC.md:299)",
                        "parallelism": f"camera-sharded x{world}", "l2": "inputs larger than L2 (no flush)",
                        "step": "a1-a9 (+a11 exchange): load+precompute+sort, visibility, assignment, block loads "
                                "at uniform cuts, crop masks", "seed": hex(sc.cfg.seed)},
