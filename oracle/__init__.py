@@ -296,3 +296,111 @@ def evaluate_cuts(scene, pre, vis, grid, mode=MODE_RATIO):
     :179 'the back-projection is computed once and reused')."""
     asg = assign(scene, pre, vis, grid)
     return block_loads(scene, pre, vis, asg, grid, mode=mode, masks=False)["objective"]
+
+
+# ------------------------------------------------------------------------------
+# NEXT-4 block pipeline (SURVEY §8f; SPEC.md:529-571; PAPER.md:156, :185-187;
+# ledger L25). Plain list operations over sub-scenes (small cases only); every
+# float operation is one numpy float32 op in the order written (no fusion).
+SUB_FIELDS = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
+
+
+def block_of_points(fr, mm, grid, x, y, z):
+    """Delta = 0 cell block p n + q of arbitrary positions (O3 map, clamped, L25)."""
+    L = lib()
+    c0, rho, au, av = fr
+    x, y, z = (np.ascontiguousarray(a, np.float32) for a in (x, y, z))
+    out = np.empty(len(x), np.int32)
+    _chk(L.oracle_block_of_points(ctypes.c_int64(len(x)), _p(x), _p(y), _p(z), _p(c0), ctypes.c_float(rho), _p(au),
+                                  _p(av), _p(np.ascontiguousarray(mm, np.float32)), grid["m"], grid["n"],
+                                  _p(grid["v"]), _p(grid["h"]), _p(out)), "block_of_points")
+    return out
+
+
+def subscene(scene, crop_b, elig_b):
+    """visibility_crop: the Gaussians of block b's crop mask in
+    ascending caller index; origin = that index; in_block = eligible bit."""
+    G = scene.G
+    idx = [i for i in range(G) if (int(crop_b[i >> 6]) >> (i & 63)) & 1]
+    sub = {k: np.array([getattr(scene, k)[i] for i in idx], np.float32) for k in SUB_FIELDS}
+    sub["origin"] = np.array(idx, np.int64)
+    sub["in_block"] = np.array([(int(elig_b[i >> 6]) >> (i & 63)) & 1 for i in idx], np.uint8)
+    return sub
+
+
+def _rot(qw, qx, qy, qz):
+    f = np.float32
+    two, one = f(2.0), f(1.0)
+    return [one - two * (qy * qy + qz * qz), two * (qx * qy - qw * qz), two * (qx * qz + qw * qy),
+            two * (qx * qy + qw * qz), one - two * (qx * qx + qz * qz), two * (qy * qz - qw * qx),
+            two * (qx * qz - qw * qy), two * (qy * qz + qw * qx), one - two * (qx * qx + qy * qy)]
+
+
+def densify_step(sub, grad, normals, tau_grad, scale_split, fr, mm, grid, b):
+    """simulate_densify_step (ledger L25). Selected: in_block and
+    grad >= tau_grad. Clone (max s < scale_split): two Gaussians at
+    mu + (0.1 s) * n_k, k = 1 keeps the origin, k = 2 gets -1. Split: two
+    children at mu + R(q) (s * n_k) with scale s / 1.6, origin -1. n_1 =
+    normals[i, 0:3], n_2 = normals[i, 3:6]. Moved / new Gaussians get a fresh
+    in-block test; everything else is copied field for field, in input order."""
+    f = np.float32
+    out = {k: [] for k in SUB_FIELDS + ("origin", "in_block")}
+    pend = []  # (out position, x, y, z) needing an in-block test
+
+    def put(vals, origin, inb):
+        for k in SUB_FIELDS:
+            out[k].append(f(vals[k]))
+        out["origin"].append(int(origin))
+        out["in_block"].append(int(inb))
+
+    for i in range(len(sub["x"])):
+        g = {k: f(sub[k][i]) for k in SUB_FIELDS}
+        if not (sub["in_block"][i] and f(grad[i]) >= f(tau_grad)):
+            put(g, sub["origin"][i], sub["in_block"][i])
+            continue
+        n = [f(v) for v in normals[i]]
+        smax = max(g["sx"], g["sy"], g["sz"])
+        for k in range(2):
+            nk = n[3 * k:3 * k + 3]
+            c = dict(g)
+            if smax < f(scale_split):  # clone: jitter by 0.1 s
+                c["x"] = g["x"] + (f(0.1) * g["sx"]) * nk[0]
+                c["y"] = g["y"] + (f(0.1) * g["sy"]) * nk[1]
+                c["z"] = g["z"] + (f(0.1) * g["sz"]) * nk[2]
+                origin = sub["origin"][i] if k == 0 else -1
+            else:  # split: sample inside the parent footprint, scale / 1.6
+                r = _rot(g["qw"], g["qx"], g["qy"], g["qz"])
+                t = [g["sx"] * nk[0], g["sy"] * nk[1], g["sz"] * nk[2]]
+                d = [(r[3 * a] * t[0] + r[3 * a + 1] * t[1]) + r[3 * a + 2] * t[2] for a in range(3)]
+                c["x"], c["y"], c["z"] = g["x"] + d[0], g["y"] + d[1], g["z"] + d[2]
+                c["sx"], c["sy"], c["sz"] = g["sx"] / f(1.6), g["sy"] / f(1.6), g["sz"] / f(1.6)
+                origin = -1
+            pend.append(len(out["x"]))
+            put(c, origin, 0)
+    res = {k: np.array(v, np.float32) for k, v in out.items() if k in SUB_FIELDS}
+    res["origin"] = np.array(out["origin"], np.int64)
+    res["in_block"] = np.array(out["in_block"], np.uint8)
+    if pend:
+        pend = np.array(pend)
+        blk = block_of_points(fr, mm, grid, res["x"][pend], res["y"][pend], res["z"][pend])
+        res["in_block"][pend] = (blk == b).astype(np.uint8)
+    return res
+
+
+def prune_outside(sub, fr, mm, grid, b):
+    """prune_outside: keep the Gaussians whose centre lies in block
+    b's delta = 0 cell (fresh test), in order."""
+    blk = block_of_points(fr, mm, grid, sub["x"], sub["y"], sub["z"])
+    keep = [i for i in range(len(blk)) if blk[i] == b]
+    res = {k: np.asarray(v)[keep] for k, v in sub.items()}
+    res["in_block"] = np.ones(len(keep), np.uint8)
+    return res
+
+
+def merge_blocks(subs):
+    """merge_blocks: concatenation in block order; a non-negative
+    origin appearing twice is an integrity error (returns (merged, ok))."""
+    res = {k: np.concatenate([np.asarray(s[k]) for s in subs]) for k in subs[0]}
+    o = res["origin"][res["origin"] >= 0]
+    ok = len(np.unique(o)) == len(o)
+    return res, ok

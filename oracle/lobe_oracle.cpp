@@ -629,4 +629,26 @@ int oracle_crop(int64_t G, const float* gu, const float* gv, int m, int n, const
   return O_OK;
 }
 
+// ------------------------------------------- NEXT-4 block pipeline (L25)
+// Block of arbitrary points (densified children, moved clones): O3's map with
+// the scene's frame and min/max, normalised coordinates clamped to [0,1]
+// (ledger L25), then the delta = 0 half-open cells (L11). block[i] = p n + q.
+int oracle_block_of_points(int64_t N, const float* x, const float* y, const float* z, const float* c0, float rho,
+                           const float* au, const float* av, const float* mm, int m, int n, const float* vcuts,
+                           const float* hcuts, int32_t* block) {
+  int st = check_grid(m, n, vcuts, hcuts, 0.0f, 0.0f, 0.0);
+  if (st) return st;
+  Axis U = make_axis(m, vcuts, 0.0f), V = make_axis(n, hcuts, 0.0f);
+  const float du = mm[1] - mm[0], dv = mm[3] - mm[2];
+  for (int64_t i = 0; i < N; ++i) {
+    float ru, rv;
+    ground_uv(x[i], y[i], z[i], c0, rho, au, av, &ru, &rv);
+    float gu = (ru - mm[0]) / du, gv = (rv - mm[2]) / dv;
+    gu = std::fmin(1.0f, std::fmax(0.0f, gu));
+    gv = std::fmin(1.0f, std::fmax(0.0f, gv));
+    block[i] = cell_of(U, gu) * n + cell_of(V, gv);
+  }
+  return O_OK;
+}
+
 }  // extern "C"
