@@ -59,7 +59,9 @@ typedef enum {
   LOBE_E_CUDA = 6,              /* CUDA runtime error or no device */
   LOBE_E_NCCL = 7,              /* reserved: collective failure reported by the exchange layer */
   LOBE_E_OOM = 8,               /* device allocation failed */
-  LOBE_E_STATE = 9              /* call out of order (e.g. combine before partial) */
+  LOBE_E_STATE = 9,             /* call out of order (e.g. combine before partial) */
+  LOBE_E_CAPACITY = 10,         /* output capacity too small (the needed count is reported) */
+  LOBE_E_INTEGRITY = 11         /* merge: an origin index appears in two blocks */
 } lobe_status;
 
 typedef struct lobe_scene lobe_scene; /* opaque */
@@ -256,6 +258,56 @@ lobe_status lobe_crop_from_masks(lobe_scene* scene, const lobe_grid* grid, const
                                  uint64_t* eligible);
 
 /* ---- introspection / tests ----------------------------------------------- */
+
+/* ---------------------------------------------------------------------------
+ * Block pipeline after the path (PAPER.md:156
+ * "prune regions outside each block and merge", :185-187 visibility cropping and
+ * selective densification; DESIGN.md ledger L25).
+ *
+ * A sub-scene: device SoA arrays of one block's Gaussians. origin: caller index
+ * of the coarse Gaussian (-1 for Gaussians created by densification);
+ * in_block: centre inside the block's delta = 0 half-open cell. Outputs are
+ * written into caller-allocated device arrays of `capacity` entries; out->n
+ * receives the count. If the count exceeds capacity nothing is written, out->n
+ * is the needed count and the call returns LOBE_E_CAPACITY. Block indices are
+ * b = p n + q of the grid (ledger L9); point-in-cell tests use the scene's
+ * frame and min/max (O3), normalised coordinates clamped to [0,1] (L25). */
+typedef struct {
+  int64_t n;
+  float *x, *y, *z, *sx, *sy, *sz, *qw, *qx, *qy, *qz, *opacity;
+  int64_t* origin;
+  uint8_t* in_block;
+} lobe_subscene;
+
+/* visibility_crop: the Gaussians of block b's crop mask M_b
+ * (visible from some camera of C^(b)) in ascending caller index,
+ * gathered from `coarse` (the loaded Gaussians, device pointers, caller order);
+ * in_block = the eligible mask bit. Single-rank scenes. */
+lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
+                                lobe_subscene* out, int64_t capacity);
+
+/* simulate_densify_step: Gaussians with in_block and
+ * grad >= tau_grad are cloned (max(s) < scale_split: two copies at
+ * mu + (0.1 s) * n_k, the first keeps its origin) or split (two children at
+ * mu + R(q)(s * n_k) with scale s / 1.6, origin -1), n_1 = normals[6 i .. 6 i + 2],
+ * n_2 = normals[6 i + 3 .. 6 i + 5] (device, caller-drawn standard normals);
+ * moved and new Gaussians get a fresh in-block test; every other Gaussian is
+ * copied field for field; output in input order (each selected Gaussian
+ * replaced in place by its two results). grad: device, in->n floats. */
+lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                              const float* grad, const float* normals, float tau_grad, float scale_split,
+                              lobe_subscene* out, int64_t capacity);
+
+/* prune_outside: the Gaussians whose centre lies in block b's
+ * delta = 0 cell (fresh test), in order; in_block = 1 for all of them. */
+lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                               lobe_subscene* out, int64_t capacity);
+
+/* merge_blocks: concatenation of `count` sub-scenes in order.
+ * LOBE_E_INTEGRITY if a non-negative origin index appears twice (the merged
+ * arrays are still written). */
+lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
+                              int64_t capacity);
 
 /* Sizes of a loaded scene without waiting for its work to finish (lobe_get_stats
  * synchronises the scene's stream to read the load-pass timings): total

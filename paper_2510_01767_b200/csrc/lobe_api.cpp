@@ -530,6 +530,67 @@ void fill_records(const lobe_scene* s, const GridV& g, const uint32_t* ncams, co
   if (objective) *objective = best;
 }
 
+// ---- NEXT-4 block pipeline helpers (ledger L25)
+CellArgs make_cell_args(const lobe_scene* s, const GridV& g) {
+  CellArgs c{};
+  for (int a = 0; a < 3; ++a) {
+    c.frame.c0[a] = s->frame.center[a];
+    c.frame.au[a] = s->frame.axis_u[a];
+    c.frame.av[a] = s->frame.axis_v[a];
+  }
+  c.frame.rho = s->frame.radius;
+  for (int k = 0; k < 4; ++k) c.mm[k] = s->mm[k];
+  c.m = g.m;
+  c.n = g.n;
+  for (int i = 0; i + 1 < g.m; ++i) c.v[i] = g.v[i];
+  for (int j = 0; j + 1 < g.n; ++j) c.h[j] = g.h[j];
+  return c;
+}
+
+SubArgs sub_args(const lobe_subscene* in) {
+  SubArgs a{};
+  const float* f[11] = {in->x, in->y, in->z, in->sx, in->sy, in->sz, in->qw, in->qx, in->qy, in->qz, in->opacity};
+  for (int k = 0; k < 11; ++k) a.f[k] = f[k];
+  return a;
+}
+
+SubOut sub_out(lobe_subscene* out) {
+  SubOut o{};
+  float* f[11] = {out->x, out->y, out->z, out->sx, out->sy, out->sz, out->qw, out->qx, out->qy, out->qz, out->opacity};
+  for (int k = 0; k < 11; ++k) o.f[k] = f[k];
+  o.origin = out->origin;
+  o.in_block = out->in_block;
+  return o;
+}
+
+lobe_status check_sub(const lobe_subscene* p, bool need_arrays, const char* what) {
+  if (!p) return fail(LOBE_E_INVALID_CONFIG, std::string(what) + " is NULL");
+  if (p->n < 0) return fail(LOBE_E_INVALID_CONFIG, std::string(what) + ": negative count");
+  if (need_arrays) {
+    const void* f[13] = {p->x, p->y, p->z, p->sx, p->sy, p->sz, p->qw, p->qx, p->qy, p->qz, p->opacity,
+                         p->origin, p->in_block};
+    for (const void* q : f)
+      if (!q) return fail(LOBE_E_INVALID_CONFIG, std::string(what) + ": NULL array");
+  }
+  return LOBE_OK;
+}
+
+// exclusive scan of cnt[0..n) into off[0..n] (off[n] = total), total returned on the host
+lobe_status scan_counts(lobe_scene* s, const uint32_t* cnt, uint32_t* off, int64_t n, uint64_t* total) {
+  cudaStream_t st = s->stream;
+  size_t tb = 0;
+  CK(exclusive_scan_u32(nullptr, tb, cnt, off, n + 1, st));
+  void* tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, tb, st));
+  CUBL(exclusive_scan_u32(tmp, tb, cnt, off, n + 1, st));
+  cudaFreeAsync(tmp, st);
+  uint32_t t = 0;
+  CK(cudaMemcpyAsync(&t, off + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *total = t;
+  return LOBE_OK;
+}
+
 // Load-pass timings and counters (events and pinned counters of the last load).
 void finalize_load_stats(lobe_scene* s) {
   if (!s->stats_pending) return;
@@ -1247,6 +1308,170 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   CK(cudaEventSynchronize(s->ev[7]));
   if (ms) *ms = ms_between(s->ev[6], s->ev[7]) / reps;
   if (grid) *grid = g;
+  return LOBE_OK;
+}
+
+lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
+                                lobe_subscene* out, int64_t capacity) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: not supported for the block pipeline");
+  if (!coarse || coarse->n != s->G || !coarse->on_device)
+    return fail(LOBE_E_INVALID_CONFIG, "coarse: the loaded Gaussians as device arrays");
+  TRY(check_sub(out, capacity > 0, "out"));
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  if (block < 0 || block >= g.B) return fail(LOBE_E_INVALID_INDEX, "block");
+  TRY(ensure_eval(s, g));
+  cudaStream_t st = s->stream;
+  const int64_t W64 = (s->G + 63) / 64;
+  uint64_t *dc = nullptr, *de = nullptr;
+  CK(s->alloc(&dc, (size_t)g.B * W64));
+  CK(s->alloc(&de, (size_t)g.B * W64));
+  {
+    uint64_t* mbits = nullptr;
+    uint8_t* cb8 = nullptr;
+    CK(s->alloc(&mbits, (size_t)s->words * 32));
+    CK(s->alloc(&cb8, (size_t)s->words * 32));
+    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
+                   reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st));
+    s->release(mbits);
+    s->release(cb8);
+  }
+  const uint64_t* cb = dc + (size_t)block * W64;
+  const uint64_t* eb = de + (size_t)block * W64;
+  uint32_t *cnt = nullptr, *off = nullptr;
+  CK(s->alloc(&cnt, (size_t)W64 + 1));
+  CK(s->alloc(&off, (size_t)W64 + 1));
+  CK(cudaMemsetAsync(cnt + W64, 0, sizeof(uint32_t), st));
+  KL(launch_mask_popc(cb, W64, cnt, st));
+  uint64_t total = 0;
+  TRY(scan_counts(s, cnt, off, W64, &total));
+  out->n = (int64_t)total;
+  lobe_status rs = LOBE_OK;
+  if ((int64_t)total > capacity) {
+    rs = fail(LOBE_E_CAPACITY, "sub-scene needs " + std::to_string(total) + " entries");
+  } else if (total > 0) {
+    SubArgs in{};
+    const float* f[11] = {coarse->x, coarse->y, coarse->z, coarse->sx, coarse->sy, coarse->sz,
+                          coarse->qw, coarse->qx, coarse->qy, coarse->qz, coarse->opacity};
+    for (int k = 0; k < 11; ++k) in.f[k] = f[k];
+    KL(launch_extract(cb, eb, W64, off, in, sub_out(out), st));
+  }
+  s->release(cnt);
+  s->release(off);
+  s->release(dc);
+  s->release(de);
+  CK(cudaStreamSynchronize(st));
+  return rs;
+}
+
+lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                              const float* grad, const float* normals, float tau_grad, float scale_split,
+                              lobe_subscene* out, int64_t capacity) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  TRY(check_sub(in, in && in->n > 0, "in"));
+  TRY(check_sub(out, capacity > 0, "out"));
+  if (in->n > 0 && (!grad || !normals)) return fail(LOBE_E_INVALID_CONFIG, "grad / normals NULL");
+  if (!std::isfinite(tau_grad) || !std::isfinite(scale_split)) return fail(LOBE_E_INVALID_CONFIG, "thresholds");
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  if (block < 0 || block >= g.B) return fail(LOBE_E_INVALID_INDEX, "block");
+  cudaStream_t st = s->stream;
+  const int64_t n = in->n;
+  uint32_t *cnt = nullptr, *off = nullptr;
+  CK(s->alloc(&cnt, (size_t)n + 1));
+  CK(s->alloc(&off, (size_t)n + 1));
+  CK(cudaMemsetAsync(cnt + n, 0, sizeof(uint32_t), st));
+  if (n > 0) KL(launch_densify_count(n, in->in_block, grad, tau_grad, cnt, st));
+  uint64_t total = 0;
+  TRY(scan_counts(s, cnt, off, n, &total));
+  out->n = (int64_t)total;
+  lobe_status rs = LOBE_OK;
+  if ((int64_t)total > capacity) rs = fail(LOBE_E_CAPACITY, "densified sub-scene needs " + std::to_string(total));
+  else if (n > 0)
+    KL(launch_densify_write(n, sub_args(in), in->origin, in->in_block, grad, normals, tau_grad, scale_split, off,
+                            make_cell_args(s, g), block, sub_out(out), st));
+  s->release(cnt);
+  s->release(off);
+  CK(cudaStreamSynchronize(st));
+  return rs;
+}
+
+lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                               lobe_subscene* out, int64_t capacity) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  TRY(check_sub(in, in && in->n > 0, "in"));
+  TRY(check_sub(out, capacity > 0, "out"));
+  CK(cudaSetDevice(s->device));
+  GridV g;
+  TRY(check_grid(grid, &g));
+  if (block < 0 || block >= g.B) return fail(LOBE_E_INVALID_INDEX, "block");
+  cudaStream_t st = s->stream;
+  const int64_t n = in->n;
+  uint32_t *cnt = nullptr, *off = nullptr;
+  CK(s->alloc(&cnt, (size_t)n + 1));
+  CK(s->alloc(&off, (size_t)n + 1));
+  CK(cudaMemsetAsync(cnt + n, 0, sizeof(uint32_t), st));
+  const CellArgs cell = make_cell_args(s, g);
+  if (n > 0) KL(launch_prune_count(n, in->x, in->y, in->z, cell, block, cnt, st));
+  uint64_t total = 0;
+  TRY(scan_counts(s, cnt, off, n, &total));
+  out->n = (int64_t)total;
+  lobe_status rs = LOBE_OK;
+  if ((int64_t)total > capacity) rs = fail(LOBE_E_CAPACITY, "pruned sub-scene needs " + std::to_string(total));
+  else if (n > 0) KL(launch_prune_write(n, sub_args(in), in->origin, cnt, off, sub_out(out), st));
+  s->release(cnt);
+  s->release(off);
+  CK(cudaStreamSynchronize(st));
+  return rs;
+}
+
+lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
+                              int64_t capacity) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (count < 0 || (count > 0 && !subs)) return fail(LOBE_E_INVALID_CONFIG, "subs");
+  TRY(check_sub(out, capacity > 0, "out"));
+  int64_t total = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    TRY(check_sub(&subs[k], subs[k].n > 0, "subs[k]"));
+    total += subs[k].n;
+  }
+  out->n = total;
+  if (total > capacity) return fail(LOBE_E_CAPACITY, "merged scene needs " + std::to_string(total));
+  CK(cudaSetDevice(s->device));
+  cudaStream_t st = s->stream;
+  uint32_t* bits = nullptr;
+  unsigned long long* dup = nullptr;
+  CK(s->alloc(&bits, (size_t)(s->G + 31) / 32 + 1));
+  CK(s->alloc(&dup, 1));
+  CK(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * ((s->G + 31) / 32 + 1), st));
+  CK(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), st));
+  int64_t pos = 0;
+  for (int32_t k = 0; k < count; ++k) {
+    const lobe_subscene& a = subs[k];
+    if (a.n == 0) continue;
+    const float* fi[11] = {a.x, a.y, a.z, a.sx, a.sy, a.sz, a.qw, a.qx, a.qy, a.qz, a.opacity};
+    float* fo[11] = {out->x, out->y, out->z, out->sx, out->sy, out->sz, out->qw, out->qx, out->qy, out->qz,
+                     out->opacity};
+    for (int f = 0; f < 11; ++f)
+      CK(cudaMemcpyAsync(fo[f] + pos, fi[f], sizeof(float) * a.n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(out->origin + pos, a.origin, sizeof(int64_t) * a.n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(out->in_block + pos, a.in_block, a.n, cudaMemcpyDeviceToDevice, st));
+    KL(launch_origin_claim(a.n, a.origin, s->G, bits, dup, st));
+    pos += a.n;
+  }
+  unsigned long long hd = ~0ull;
+  CK(cudaMemcpyAsync(&hd, dup, sizeof(hd), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s->release(bits);
+  s->release(dup);
+  if (hd != ~0ull) return fail(LOBE_E_INTEGRITY, "origin index " + std::to_string(hd) + " appears twice (SPEC.md:569)");
   return LOBE_OK;
 }
 

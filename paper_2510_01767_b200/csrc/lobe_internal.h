@@ -191,4 +191,34 @@ cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* 
 cudaError_t launch_gblk(const ZoneTables* dz, int nzv, int nzp, const uint32_t* zp_count, uint32_t* gblk,
                         cudaStream_t st);
 
+// ---- NEXT-4 block pipeline (ledger L25) -------------------------------------
+struct SubArgs {  // 11 input float fields: x y z sx sy sz qw qx qy qz opacity
+  const float* f[11];
+};
+struct SubOut {
+  float* f[11];
+  int64_t* origin;
+  uint8_t* in_block;
+};
+struct CellArgs {  // delta = 0 cell of a position: frame (O3), min/max, cuts
+  PrepIn frame;    // only c0, rho, au, av are used
+  float mm[4];
+  int m, n;
+  float v[64], h[64];
+};
+cudaError_t launch_mask_popc(const uint64_t* mask, int64_t W64, uint32_t* cnt, cudaStream_t st);
+cudaError_t launch_extract(const uint64_t* crop, const uint64_t* elig, int64_t W64, const uint32_t* off,
+                           const SubArgs& in, const SubOut& out, cudaStream_t st);
+cudaError_t launch_densify_count(int64_t n, const uint8_t* in_block, const float* grad, float tau, uint32_t* cnt,
+                                 cudaStream_t st);
+cudaError_t launch_densify_write(int64_t n, const SubArgs& in, const int64_t* origin, const uint8_t* in_block,
+                                 const float* grad, const float* normals, float tau, float split, const uint32_t* off,
+                                 const CellArgs& cell, int block, const SubOut& out, cudaStream_t st);
+cudaError_t launch_prune_count(int64_t n, const float* x, const float* y, const float* z, const CellArgs& cell,
+                               int block, uint32_t* cnt, cudaStream_t st);
+cudaError_t launch_prune_write(int64_t n, const SubArgs& in, const int64_t* origin, const uint32_t* cnt,
+                               const uint32_t* off, const SubOut& out, cudaStream_t st);
+cudaError_t launch_origin_claim(int64_t n, const int64_t* origin, int64_t G, uint32_t* bits, unsigned long long* dup,
+                                cudaStream_t st);
+
 }  // namespace lobe

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "liblobe.so")
 
 STATUS = {0: "OK", 1: "INVALID_INPUT", 2: "INVALID_CONFIG", 3: "INVALID_CUTS", 4: "INVALID_INDEX",
-          5: "DEGENERATE_SCENE", 6: "CUDA", 7: "NCCL", 8: "OOM", 9: "STATE"}
+          5: "DEGENERATE_SCENE", 6: "CUDA", 7: "NCCL", 8: "OOM", 9: "STATE", 10: "CAPACITY", 11: "INTEGRITY"}
 ASSIGN_RATIO, ASSIGN_HOME, ASSIGN_UNION = 0, 1, 2
 FRAME_AUTO_CENTER, FRAME_AUTO_RADIUS, FRAME_AUTO_AXES, FRAME_AUTO_ALL = 1, 2, 4, 7
 
@@ -23,7 +23,8 @@ FRAME_AUTO_CENTER, FRAME_AUTO_RADIUS, FRAME_AUTO_AXES, FRAME_AUTO_ALL = 1, 2, 4,
 EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign_cameras", "lobe_block_loads",
            "lobe_crop_masks", "lobe_balance_partition", "lobe_bo_run", "lobe_mask_words", "lobe_block_partial",
            "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
-           "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench"]
+           "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench", "lobe_block_subscene",
+           "lobe_densify_step", "lobe_prune_outside", "lobe_merge_blocks"]
 
 
 PREDICATE_ISOTROPIC, PREDICATE_ANISOTROPIC = 0, 1  # lobe_options.predicate (DESIGN.md ledger L24)
@@ -40,6 +41,32 @@ class Gaussians(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64)] + [(k, ctypes.c_void_p) for k in
                                            ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")] + \
                [("on_device", ctypes.c_int32)]
+
+
+SUB_FIELDS = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
+
+
+class SubScene(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64)] + [(k, ctypes.c_void_p) for k in SUB_FIELDS] + \
+               [("origin", ctypes.c_void_p), ("in_block", ctypes.c_void_p)]
+
+
+def _sub_alloc(cap, device):
+    """Device arrays (torch) for a sub-scene of capacity `cap`."""
+    import torch
+    cap = max(int(cap), 1)
+    d = {k: torch.empty(cap, dtype=torch.float32, device=device) for k in SUB_FIELDS}
+    d["origin"] = torch.empty(cap, dtype=torch.int64, device=device)
+    d["in_block"] = torch.empty(cap, dtype=torch.uint8, device=device)
+    return d
+
+
+def _sub_struct(d, n):
+    return SubScene(int(n), *[_ptr(d[k]) for k in SUB_FIELDS], _ptr(d["origin"]), _ptr(d["in_block"]))
+
+
+def _sub_result(d, st):
+    return {k: v[:st.n] for k, v in d.items()}
 
 
 class Camera(ctypes.Structure):
@@ -118,6 +145,13 @@ def lib():
         L.lobe_balance_partition.argtypes = [vp, i32, i32, ctypes.POINTER(BalanceOpts), vp, vp, vp, vp, vp]
         L.lobe_bo_run.argtypes = [i32, i32, ctypes.POINTER(BalanceOpts), OBJECTIVE_FN, vp, vp, vp, vp, vp]
         L.lobe_block_partial.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
+        L.lobe_scene_info.argtypes = [vp, vp, vp, vp, vp]
+        SP = ctypes.POINTER(SubScene)
+        L.lobe_block_subscene.argtypes = [vp, ctypes.POINTER(Grid), i32, ctypes.POINTER(Gaussians), SP, i64]
+        L.lobe_densify_step.argtypes = [vp, ctypes.POINTER(Grid), i32, SP, vp, vp, ctypes.c_float, ctypes.c_float,
+                                        SP, i64]
+        L.lobe_prune_outside.argtypes = [vp, ctypes.POINTER(Grid), i32, SP, SP, i64]
+        L.lobe_merge_blocks.argtypes = [vp, SP, i32, SP, i64]
         L.lobe_masks_combine.argtypes = [vp, i32, vp, i32, vp, vp]
         L.lobe_block_records.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp, vp, vp]
         L.lobe_crop_from_masks.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
@@ -293,6 +327,52 @@ class Scene:
         _check(lib().lobe_balance_partition(self.handle, m, n, ctypes.byref(o), _ptr(v), _ptr(h), _ptr(hist),
                                             _ptr(ch), recs))
         return dict(v=v[:m - 1], h=h[:n - 1], history=hist, cut_history=ch[:, :D], best=records_to_dict(recs, None))
+
+    # ---- block pipeline ----------------------
+    def block_subscene(self, m, n, block, coarse, device="cuda", **grid_kw):
+        """The crop sub-scene of `block` (dict of device tensors; origin, in_block)."""
+        g, keep = make_grid(m, n, **grid_kw)
+        arrs = [getattr(coarse, k) for k in SUB_FIELDS]
+        cg = Gaussians(int(arrs[0].shape[0]), *[_ptr(a) for a in arrs], 1)
+        d = _sub_alloc(self.G, device)
+        st = _sub_struct(d, 0)
+        _check(lib().lobe_block_subscene(self.handle, ctypes.byref(g), int(block), ctypes.byref(cg),
+                                         ctypes.byref(st), int(self.G)))
+        return _sub_result(d, st)
+
+    def densify_step(self, m, n, block, sub, grad, normals, tau_grad, scale_split, device="cuda", **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        nin = int(sub["x"].shape[0])
+        si = _sub_struct(sub, nin)
+        d = _sub_alloc(2 * nin, device)
+        so = _sub_struct(d, 0)
+        _check(lib().lobe_densify_step(self.handle, ctypes.byref(g), int(block), ctypes.byref(si), _ptr(grad),
+                                       _ptr(normals), ctypes.c_float(tau_grad), ctypes.c_float(scale_split),
+                                       ctypes.byref(so), int(max(2 * nin, 1))))
+        return _sub_result(d, so)
+
+    def prune_outside(self, m, n, block, sub, device="cuda", **grid_kw):
+        g, keep = make_grid(m, n, **grid_kw)
+        nin = int(sub["x"].shape[0])
+        si = _sub_struct(sub, nin)
+        d = _sub_alloc(nin, device)
+        so = _sub_struct(d, 0)
+        _check(lib().lobe_prune_outside(self.handle, ctypes.byref(g), int(block), ctypes.byref(si),
+                                        ctypes.byref(so), int(max(nin, 1))))
+        return _sub_result(d, so)
+
+    def merge_blocks(self, subs, device="cuda"):
+        """Concatenation in order; raises LobeError(INTEGRITY) on a duplicated origin."""
+        arr = (SubScene * max(len(subs), 1))()
+        tot = 0
+        for k, sb in enumerate(subs):
+            nk = int(sb["x"].shape[0])
+            arr[k] = _sub_struct(sb, nk)
+            tot += nk
+        d = _sub_alloc(tot, device)
+        so = _sub_struct(d, 0)
+        _check(lib().lobe_merge_blocks(self.handle, arr, len(subs), ctypes.byref(so), int(max(tot, 1))))
+        return _sub_result(d, so)
 
     def export_rows(self, c0=0, count=None):
         count = self.n_local - c0 if count is None else count
