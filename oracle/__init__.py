@@ -404,3 +404,67 @@ def merge_blocks(subs):
     o = res["origin"][res["origin"] >= 0]
     ok = len(np.unique(o)) == len(o)
     return res, ok
+
+
+# ------------------------------------------------------------------------------
+# NEXT-1 paper-exact camera selection (
+# SPEC.md:335-353, :383-387; ledger L26): alpha-blended depth render of each
+# camera's visible Gaussians at 1/downscale resolution, back-projection of every
+# stride-th pixel with weight >= eps_w, V_{c,b} ratios over the clouds.
+def render_camera(scene, pre, fr, c, vis_idx, downscale=4, stride=2, eps_w=0.1):
+    """One camera: returns (D map, W map, cloud gu, cloud gv)."""
+    L = lib()
+    c0, rho, au, av = fr
+    cv = pre.get("cov")
+    if cv is None:
+        cv = pre["cov"] = cov(scene)
+    cams = _cams(scene)
+    Wd, Hd = int(scene.width[c]) // downscale, int(scene.height[c]) // downscale
+    D = np.zeros((Hd, Wd), np.float32)
+    W = np.zeros((Hd, Wd), np.float32)
+    cap = max(1, -(-Hd // stride) * -(-Wd // stride))
+    pu = np.empty(cap, np.float32)
+    pv = np.empty(cap, np.float32)
+    K = ctypes.c_int64()
+    vis_idx = np.ascontiguousarray(vis_idx, np.int64)
+    _chk(L.oracle_render_camera(ctypes.c_int64(scene.G), _p(scene.x), _p(scene.y), _p(scene.z), _p(cv),
+                                _p(scene.opacity), ctypes.byref(cams[c]), ctypes.c_int64(len(vis_idx)), _p(vis_idx),
+                                ctypes.c_int(downscale), ctypes.c_int(stride), ctypes.c_float(eps_w), _p(c0),
+                                ctypes.c_float(rho), _p(au), _p(av), _p(np.ascontiguousarray(pre["minmax"])),
+                                _p(D), _p(W), _p(pu), _p(pv), ctypes.byref(K)), "render_camera")
+    return D, W, pu[:K.value].copy(), pv[:K.value].copy()
+
+
+def render_clouds(scene, pre, vis, fr, downscale=4, stride=2, eps_w=0.1):
+    """All cameras: CSR clouds {off, gu, gv} from the visibility rows' sets."""
+    G = scene.G
+    rows = vis["rows"]
+    bits = np.unpackbits(rows.view(np.uint8), bitorder="little").reshape(rows.shape[0], -1)[:, :G]
+    off = [0]
+    us, vs = [], []
+    for c in range(rows.shape[0]):
+        _, _, pu, pv = render_camera(scene, pre, fr, c, np.flatnonzero(bits[c]), downscale, stride, eps_w)
+        us.append(pu)
+        vs.append(pv)
+        off.append(off[-1] + len(pu))
+    return dict(off=np.array(off, np.int64), gu=np.concatenate(us) if us else np.zeros(0, np.float32),
+                gv=np.concatenate(vs) if vs else np.zeros(0, np.float32))
+
+
+def assign_points(scene, pre, clouds, grid):
+    """O8 over the back-projected clouds: V_{c,b} = n / K >= tau."""
+    L = lib()
+    m, n = grid["m"], grid["n"]
+    B = m * n
+    ns = len(clouds["off"]) - 1
+    ncb = np.empty((ns, B), np.uint32)
+    n0 = np.empty((ns, B), np.uint32)
+    member = np.empty(ns, np.uint64)
+    home = np.empty(ns, np.int32)
+    _chk(L.oracle_assign_points(ctypes.c_int64(ns), _p(clouds["off"]), _p(clouds["gu"]), _p(clouds["gv"]),
+                                _p(pre["cam_gu"]), _p(pre["cam_gv"]), ctypes.c_int(m), ctypes.c_int(n),
+                                _p(grid["v"]), _p(grid["h"]), ctypes.c_float(grid["dv"]), ctypes.c_float(grid["dh"]),
+                                ctypes.c_double(grid["tau"]), _p(ncb), _p(n0), _p(member), _p(home)),
+         "assign_points")
+    K = np.diff(clouds["off"]).astype(np.uint32)
+    return dict(n=ncb, n0=n0, member=member, home=home, K=K)

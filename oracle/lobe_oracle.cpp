@@ -651,4 +651,175 @@ int oracle_block_of_points(int64_t N, const float* x, const float* y, const floa
   return O_OK;
 }
 
+// ------------------------------------- NEXT-1 depth-render camera selection (L26)
+// SURVEY §8f NEXT-1; PAPER.md:175-179 (alpha-blended depth D = sum d_i a_i
+// prod_{j<i}(1 - a_j), back-projected to a point cloud, V_{c,b} ratios);
+// SPEC.md:335-353, :383-387 (downscale 4, stride 2, weight floor 0.1,
+// front-to-back by centre depth, EWA covariance + 0.3 px^2, stop at T < 1e-4).
+//
+// exp for the footprint weight, x in [-4.5, 0]: 2^n p(r), n = nearest(x log2 e),
+// r = x - n ln2 (two-step Cody-Waite), p = degree-7 Taylor polynomial in Horner
+// form with fmaf; the scaling by 2^n is exact (ledger L26).
+float exp_l26(float x) {
+  const float n = std::nearbyintf(x * 1.44269504f);
+  float r = std::fmaf(n, -0.693145752f, x);
+  r = std::fmaf(n, -1.42860677e-06f, r);
+  float p = 1.98412701e-04f;
+  p = std::fmaf(p, r, 1.38888892e-03f);
+  p = std::fmaf(p, r, 8.33333377e-03f);
+  p = std::fmaf(p, r, 4.16666679e-02f);
+  p = std::fmaf(p, r, 1.66666672e-01f);
+  p = std::fmaf(p, r, 0.5f);
+  p = std::fmaf(p, r, 1.0f);
+  p = std::fmaf(p, r, 1.0f);
+  return std::ldexp(p, (int)n);
+}
+
+// Render one camera at 1/ds resolution from its visible Gaussians (vis: caller
+// indices, any order; sorted here by (zc, index)), then back-project every
+// stride-th pixel (row-major) with weight >= eps_w. Per Gaussian (O6a's
+// sequence with fx' = fx/ds, fy' = fy/ds, cx' = cx/ds, cy' = cy/ds): upix, vpix,
+// A, B, C; det = A C - B B (skip if det <= 0); conic ca = C/det, cb = -(B/det),
+// cc = A/det. Per pixel centre (px + 0.5, py + 0.5): dx = px + 0.5 - upix,
+// dy likewise, power = -0.5 ((ca dx) dx + (cc dy) dy) - (cb dx) dy; a Gaussian
+// contributes iff power >= -4.5 (inside its 3-sigma ellipse):
+// alpha = o exp_l26(min(power, 0)); w = alpha T; D += zc w; W += w;
+// T *= (1 - alpha); stop when T < 1e-4. Back-projection: xn = (u - cx')/fx',
+// yn = (v - cy')/fy', Pc = (xn D, yn D, D), world_k = fma(R0k, q0, fma(R1k, q1,
+// R2k q2)) with q = Pc - t, then O3's map, min/max normalisation, clamp to [0,1].
+// Outputs: D, W maps (H' x W', W' = width / ds), cloud points (pu, pv, up to
+// ceil(H'/stride) ceil(W'/stride)), *K.
+int oracle_render_camera(int64_t G, const float* x, const float* y, const float* z, const float* cov,
+                         const float* o, const Cam* cam, int64_t nvis, const int64_t* vis, int ds, int stride,
+                         float eps_w, const float* c0, float rho, const float* au, const float* av, const float* mm,
+                         float* Dmap, float* Wmap, float* pu, float* pv, int64_t* K) {
+  const Cam& k = *cam;
+  const float* R = k.R;
+  const float fx = k.fx / (float)ds, fy = k.fy / (float)ds, cx = k.cx / (float)ds, cy = k.cy / (float)ds;
+  const int Wd = k.width / ds, Hd = k.height / ds;
+  struct Rec { float zc; int64_t i; float up, vp, ca, cb, cc, o; bool ok; };
+  std::vector<Rec> g(nvis);
+  for (int64_t n = 0; n < nvis; ++n) {
+    const int64_t i = vis[n];
+    Rec& e = g[n];
+    e.i = i;
+    const float xc = std::fmaf(R[0], x[i], std::fmaf(R[1], y[i], std::fmaf(R[2], z[i], k.t[0])));
+    const float yc = std::fmaf(R[3], x[i], std::fmaf(R[4], y[i], std::fmaf(R[5], z[i], k.t[1])));
+    const float zc = std::fmaf(R[6], x[i], std::fmaf(R[7], y[i], std::fmaf(R[8], z[i], k.t[2])));
+    e.zc = zc;
+    const float iz = 1.0f / zc;
+    const float a = xc * iz, b = yc * iz;
+    e.up = std::fmaf(fx, a, cx);
+    e.vp = std::fmaf(fy, b, cy);
+    const float j00 = fx * iz, j11 = fy * iz;
+    const float j02 = -(j00 * a), j12 = -(j11 * b);
+    float T0[3], T1[3];
+    for (int q = 0; q < 3; ++q) {
+      T0[q] = std::fmaf(j00, R[q], j02 * R[6 + q]);
+      T1[q] = std::fmaf(j11, R[3 + q], j12 * R[6 + q]);
+    }
+    const float* cv = cov + 6 * i;
+    const float Sg[3][3] = {{cv[0], cv[1], cv[2]}, {cv[1], cv[3], cv[4]}, {cv[2], cv[4], cv[5]}};
+    float V0[3], V1[3];
+    for (int q = 0; q < 3; ++q) {
+      V0[q] = std::fmaf(Sg[q][0], T0[0], std::fmaf(Sg[q][1], T0[1], Sg[q][2] * T0[2]));
+      V1[q] = std::fmaf(Sg[q][0], T1[0], std::fmaf(Sg[q][1], T1[1], Sg[q][2] * T1[2]));
+    }
+    const float A = std::fmaf(T0[0], V0[0], std::fmaf(T0[1], V0[1], T0[2] * V0[2])) + 0.3f;
+    const float B = std::fmaf(T1[0], V0[0], std::fmaf(T1[1], V0[1], T1[2] * V0[2]));
+    const float C = std::fmaf(T1[0], V1[0], std::fmaf(T1[1], V1[1], T1[2] * V1[2])) + 0.3f;
+    const float p1 = A * C, p2 = B * B;
+    const float det = p1 - p2;
+    e.ok = det > 0.0f;
+    e.ca = C / det;
+    e.cb = -(B / det);
+    e.cc = A / det;
+    e.o = o[i];
+  }
+  std::stable_sort(g.begin(), g.end(), [](const Rec& a, const Rec& b) {
+    return a.zc < b.zc || (a.zc == b.zc && a.i < b.i);
+  });
+  for (int py = 0; py < Hd; ++py)
+    for (int px = 0; px < Wd; ++px) {
+      float D = 0.0f, Wt = 0.0f, T = 1.0f;
+      const float u = (float)px + 0.5f, v = (float)py + 0.5f;
+      for (const Rec& e : g) {
+        if (!e.ok) continue;
+        const float dx = u - e.up, dy = v - e.vp;
+        const float t1 = (e.ca * dx) * dx, t2 = (e.cc * dy) * dy, t3 = (e.cb * dx) * dy;
+        const float power = -0.5f * (t1 + t2) - t3;
+        if (!(power >= -4.5f)) continue;
+        const float alpha = e.o * exp_l26(std::fmin(power, 0.0f));
+        const float w = alpha * T;
+        D = D + e.zc * w;
+        Wt = Wt + w;
+        T = T * (1.0f - alpha);
+        if (T < 1e-4f) break;
+      }
+      Dmap[(int64_t)py * Wd + px] = D;
+      Wmap[(int64_t)py * Wd + px] = Wt;
+    }
+  int64_t cnt = 0;
+  const float du = mm[1] - mm[0], dvv = mm[3] - mm[2];
+  for (int py = 0; py < Hd; py += stride)
+    for (int px = 0; px < Wd; px += stride) {
+      const float Wt = Wmap[(int64_t)py * Wd + px];
+      if (!(Wt >= eps_w)) continue;
+      const float D = Dmap[(int64_t)py * Wd + px];
+      const float u = (float)px + 0.5f, v = (float)py + 0.5f;
+      const float xn = (u - cx) / fx, yn = (v - cy) / fy;
+      const float q0 = xn * D - k.t[0], q1 = yn * D - k.t[1], q2 = D - k.t[2];
+      const float wx = std::fmaf(R[0], q0, std::fmaf(R[3], q1, R[6] * q2));
+      const float wy = std::fmaf(R[1], q0, std::fmaf(R[4], q1, R[7] * q2));
+      const float wz = std::fmaf(R[2], q0, std::fmaf(R[5], q1, R[8] * q2));
+      float ru, rv;
+      ground_uv(wx, wy, wz, c0, rho, au, av, &ru, &rv);
+      float gu = (ru - mm[0]) / du, gv = (rv - mm[2]) / dvv;
+      pu[cnt] = std::fmin(1.0f, std::fmax(0.0f, gu));
+      pv[cnt] = std::fmin(1.0f, std::fmax(0.0f, gv));
+      ++cnt;
+    }
+  *K = cnt;
+  return O_OK;
+}
+
+// O8 over explicit point clouds (CSR off[0..ns]): n over the enlarged regions,
+// n0 over the delta = 0 cells, member iff K > 0 and (double)n >= tau (double)K,
+// home = lowest argmax n0 (K = 0: the camera centre's cell).
+int oracle_assign_points(int64_t ns, const int64_t* off, const float* pu, const float* pv, const float* cam_gu,
+                         const float* cam_gv, int m, int n, const float* vcuts, const float* hcuts, float dv, float dh,
+                         double tau, uint32_t* ncb, uint32_t* n0cb, uint64_t* member, int32_t* home) {
+  int st = check_grid(m, n, vcuts, hcuts, dv, dh, tau);
+  if (st) return st;
+  const int B = m * n;
+  Axis U = make_axis(m, vcuts, dv), V = make_axis(n, hcuts, dh);
+  for (int64_t j = 0; j < ns; ++j) {
+    uint32_t* nj = ncb + j * B;
+    uint32_t* n0j = n0cb + j * B;
+    for (int b = 0; b < B; ++b) nj[b] = n0j[b] = 0;
+    const int64_t K = off[j + 1] - off[j];
+    for (int64_t e = off[j]; e < off[j + 1]; ++e)
+      for (int p = 0; p < m; ++p)
+        for (int q = 0; q < n; ++q) {
+          if (in_interval(pu[e], U.elo[p], U.ehi[p]) && in_interval(pv[e], V.elo[q], V.ehi[q])) nj[p * n + q] += 1;
+          if (in_interval(pu[e], U.lo[p], U.hi[p]) && in_interval(pv[e], V.lo[q], V.hi[q])) n0j[p * n + q] += 1;
+        }
+    uint64_t mem = 0;
+    if (K > 0)
+      for (int b = 0; b < B; ++b)
+        if ((double)nj[b] >= tau * (double)K) mem |= (uint64_t)1 << b;
+    member[j] = mem;
+    int hb;
+    if (K > 0) {
+      hb = 0;
+      for (int b = 1; b < B; ++b)
+        if (n0j[b] > n0j[hb]) hb = b;
+    } else {
+      hb = cell_of(U, cam_gu[j]) * n + cell_of(V, cam_gv[j]);
+    }
+    home[j] = hb;
+  }
+  return O_OK;
+}
+
 }  // extern "C"
