@@ -309,6 +309,28 @@ lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t blo
 lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
                               int64_t capacity);
 
+/* ---------------------------------------------------------------------------
+ * Paper-exact camera selection (SPEC.md:
+ * 335-353, :383-387; DESIGN.md ledger L26). Renders, for every local camera, the
+ * alpha-blended depth D = sum d_i a_i prod_{j<i}(1 - a_j) of its visible Gaussians
+ * (EWA splats, front to back by centre depth, 3-sigma support, stop at
+ * T < 1e-4) at 1/downscale resolution, back-projects every stride-th pixel with
+ * weight >= eps_w to the ground grid and from then on assigns cameras by the
+ * fraction of their cloud points inside each enlarged block (V_{c,b} >= tau,
+ * K_c = cloud size) in every lobe_assign_cameras / lobe_block_loads /
+ * lobe_balance_partition call; visibility rows, depth statistic and G_vis are
+ * unchanged. coarse: the loaded Gaussians as device arrays (their rotations and
+ * scales give the splats). downscale <= 0 -> 4, stride <= 0 -> 2, eps_w < 0 -> 0.1. */
+lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
+                               float eps_w);
+/* The clouds of the last lobe_render_select: offsets[N_local + 1] (host),
+ * gu / gv (host or device, capacity entries), camera-major, row-major samples. */
+lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity);
+/* Depth and weight maps of one local camera ((height / ds) x (width / ds) floats,
+ * host or device), rendered as lobe_render_select does. */
+lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
+                             float* depth, float* weight);
+
 /* Sizes of a loaded scene without waiting for its work to finish (lobe_get_stats
  * synchronises the scene's stream to read the load-pass timings): total
  * Gaussians and cameras, this rank's camera count and first camera. Any output

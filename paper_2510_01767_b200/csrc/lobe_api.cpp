@@ -117,6 +117,15 @@ struct lobe_scene {
   unsigned long long* queue = nullptr;
   int64_t n_sub = 0;
   uint32_t* K = nullptr;
+  // NEXT-1 (ledger L26): back-projected clouds of the local cameras; when
+  // cloud_mode is set the assignment (a6/a7) counts cloud points instead of
+  // visible Gaussians and K_c is the cloud size
+  bool cloud_mode = false;
+  float *cloud_gu = nullptr, *cloud_gv = nullptr;
+  uint32_t* cloud_cam = nullptr;
+  uint32_t* cloud_K = nullptr;
+  int64_t n_cloud = 0;
+  std::vector<lobe_camera> host_cams;  // the local cameras (render selection)
   double* D = nullptr;
   float *zmin = nullptr, *zmax = nullptr;
   uint32_t *tile_off = nullptr, *pair_cam = nullptr, *pair_tile = nullptr;
@@ -428,8 +437,11 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
   if (s->N_loc > 0) {
     CK(cudaMemsetAsync(s->hist, 0, sizeof(uint32_t) * (size_t)s->N_loc * nzp, st));
-    KL(launch_hist(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, s->zp, s->word_zone, s->tile_zone, nzp,
-                   s->hist, st));
+    if (s->cloud_mode)
+      KL(launch_hist_points(s->n_cloud, s->cloud_gu, s->cloud_gv, s->cloud_cam, s->dz, nzv, nzp, s->hist, st));
+    else
+      KL(launch_hist(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, s->zp, s->word_zone, s->tile_zone,
+                     nzp, s->hist, st));
   }
   CK(cudaEventRecord(s->ev[3], st));
   // ---- a7 assignment
@@ -438,7 +450,7 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
     a.dz = s->dz;
     a.hist = s->hist;
     a.nzp = nzp;
-    a.K = s->K;
+    a.K = s->cloud_mode ? s->cloud_K : s->K;
     a.cam_gu = s->d_cam_gu;
     a.cam_gv = s->d_cam_gv;
     a.n_cams = s->N_loc;
@@ -591,6 +603,180 @@ lobe_status scan_counts(lobe_scene* s, const uint32_t* cnt, uint32_t* off, int64
   return LOBE_OK;
 }
 
+lobe_status copy_out(lobe_scene* s, void* dst, const void* src, size_t bytes);
+
+// ---- NEXT-1 depth-render camera selection (ledger L26)
+struct RenderJob {
+  int ds = 4, stride = 2;
+  float eps_w = 0.1f;
+  // clouds appended here (device; grown as needed)
+  float *gu = nullptr, *gv = nullptr;
+  uint32_t* cam = nullptr;
+  int64_t n = 0, cap = 0;
+  // optional: maps of the batch's first camera copied here (host or device)
+  float *Dout = nullptr, *Wout = nullptr;
+};
+
+lobe_status grow_cloud(lobe_scene* s, RenderJob& J, int64_t need) {
+  if (need <= J.cap) return LOBE_OK;
+  const int64_t cap = std::max<int64_t>(need, J.cap * 2);
+  float *gu = nullptr, *gv = nullptr;
+  uint32_t* cam = nullptr;
+  CK(s->alloc(&gu, (size_t)cap));
+  CK(s->alloc(&gv, (size_t)cap));
+  CK(s->alloc(&cam, (size_t)cap));
+  if (J.n > 0) {
+    CK(cudaMemcpyAsync(gu, J.gu, sizeof(float) * J.n, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(gv, J.gv, sizeof(float) * J.n, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(cam, J.cam, sizeof(uint32_t) * J.n, cudaMemcpyDeviceToDevice, s->stream));
+  }
+  s->release(J.gu);
+  s->release(J.gv);
+  s->release(J.cam);
+  J.gu = gu;
+  J.gv = gv;
+  J.cam = cam;
+  J.cap = cap;
+  return LOBE_OK;
+}
+
+// Render cameras [c0, c1) of the local shard and append their clouds.
+lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, const std::vector<uint32_t>& hoff,
+                         const std::vector<lobe_camera>& hcams, int64_t c0, int64_t c1, RenderJob& J) {
+  cudaStream_t st = s->stream;
+  const int ncam = (int)(c1 - c0);
+  // cameras at 1/ds resolution
+  std::vector<RenderCam> rc(ncam);
+  uint32_t tiles = 0;
+  int64_t maps = 0;
+  int max_tiles = 0, max_samples = 0;
+  std::vector<uint32_t> sp0(ncam + 1, 0);
+  for (int q = 0; q < ncam; ++q) {
+    const lobe_camera& k = hcams[c0 + q];
+    RenderCam& r = rc[q];
+    for (int e = 0; e < 9; ++e) r.R[e] = k.R[e];
+    for (int e = 0; e < 3; ++e) r.t[e] = k.t[e];
+    r.fx = k.fx / (float)J.ds;
+    r.fy = k.fy / (float)J.ds;
+    r.cx = k.cx / (float)J.ds;
+    r.cy = k.cy / (float)J.ds;
+    r.Wd = k.width / J.ds;
+    r.Hd = k.height / J.ds;
+    r.tw = (r.Wd + 15) / 16;
+    r.th = (r.Hd + 15) / 16;
+    r.tile0 = tiles;
+    r.cam = (uint32_t)(c0 + q);
+    r.map0 = maps;
+    tiles += (uint32_t)(r.tw * r.th);
+    maps += (int64_t)r.Wd * r.Hd;
+    max_tiles = std::max(max_tiles, r.tw * r.th);
+    const int sw = (r.Wd + J.stride - 1) / J.stride, sh = (r.Hd + J.stride - 1) / J.stride;
+    sp0[q + 1] = sp0[q] + (uint32_t)(sw * sh);
+    max_samples = std::max(max_samples, sw * sh);
+  }
+  RenderCam* drc = nullptr;
+  CK(s->alloc(&drc, (size_t)ncam));
+  CK(cudaMemcpyAsync(drc, rc.data(), sizeof(RenderCam) * ncam, cudaMemcpyHostToDevice, st));
+  // 1. records: the visible Gaussians of the batch's non-empty pairs (camera-major)
+  const int64_t k0 = hoff[c0], nk = (int64_t)hoff[c1] - k0;
+  uint32_t *cnt = nullptr, *pos = nullptr;
+  CK(s->alloc(&cnt, (size_t)nk + 1));
+  CK(s->alloc(&pos, (size_t)nk + 1));
+  CK(cudaMemsetAsync(cnt + nk, 0, sizeof(uint32_t), st));
+  KL(launch_rvis_count(k0, nk, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, cnt, st));
+  uint64_t n = 0;
+  TRY(scan_counts(s, cnt, pos, nk, &n));
+  std::vector<uint32_t> hpos(nk + 1);
+  CK(cudaMemcpyAsync(hpos.data(), pos, sizeof(uint32_t) * (nk + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint32_t> seg(ncam + 1);
+  for (int q = 0; q <= ncam; ++q) seg[q] = hpos[hoff[c0 + q] - k0];
+  unsigned long long *keys = nullptr, *keys_s = nullptr;
+  uint32_t *vals = nullptr, *vals_s = nullptr, *rcam = nullptr, *dseg = nullptr;
+  float* rec = nullptr;
+  const size_t N1 = std::max<uint64_t>(n, 1);
+  CK(s->alloc(&keys, N1)); CK(s->alloc(&keys_s, N1));
+  CK(s->alloc(&vals, N1)); CK(s->alloc(&vals_s, N1));
+  CK(s->alloc(&rcam, N1));
+  CK(s->alloc(&rec, N1 * 10));
+  CK(s->alloc(&dseg, (size_t)ncam + 1));
+  CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
+  KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, perm, g, drc,
+                      keys, vals, rec, rcam, st));
+  // 2. front to back per camera: (zc, caller index)
+  if (n > 0) {
+    size_t tb = 0;
+    CK(seg_sort_u64(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tb, st));
+    CUBL(seg_sort_u64(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
+    cudaFreeAsync(tmp, st);
+  }
+  s->release(keys); s->release(keys_s); s->release(vals); s->release(cnt); s->release(pos);
+  // 3. tile binning in front-to-back order (stable key sort keeps it)
+  uint32_t *c2 = nullptr, *o2 = nullptr;
+  CK(s->alloc(&c2, N1 + 1));
+  CK(s->alloc(&o2, N1 + 1));
+  CK(cudaMemsetAsync(c2 + n, 0, sizeof(uint32_t), st));
+  KL(launch_bin_count((int64_t)n, vals_s, rec, rcam, drc, c2, st));
+  uint64_t E = 0;
+  TRY(scan_counts(s, c2, o2, (int64_t)n, &E));
+  uint32_t *ek = nullptr, *ev = nullptr, *ek_s = nullptr, *ev_s = nullptr;
+  const size_t E1 = std::max<uint64_t>(E, 1);
+  CK(s->alloc(&ek, E1)); CK(s->alloc(&ev, E1)); CK(s->alloc(&ek_s, E1)); CK(s->alloc(&ev_s, E1));
+  KL(launch_bin_fill((int64_t)n, vals_s, rec, rcam, drc, o2, ek, ev, st));
+  int bits = 1;
+  while ((1ull << bits) < (unsigned long long)tiles) ++bits;
+  if (E > 0) {
+    size_t tb = 0;
+    CK(sort_u32_pairs(nullptr, tb, ek, ek_s, ev, ev_s, (int64_t)E, bits, st));
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tb, st));
+    CUBL(sort_u32_pairs(tmp, tb, ek, ek_s, ev, ev_s, (int64_t)E, bits, st));
+    cudaFreeAsync(tmp, st);
+  }
+  s->release(ek); s->release(ev); s->release(c2); s->release(o2);
+  uint32_t *ts = nullptr, *te = nullptr;
+  CK(s->alloc(&ts, (size_t)tiles + 1));
+  CK(s->alloc(&te, (size_t)tiles + 1));
+  CK(cudaMemsetAsync(ts, 0, sizeof(uint32_t) * (tiles + 1), st));
+  CK(cudaMemsetAsync(te, 0, sizeof(uint32_t) * (tiles + 1), st));
+  KL(launch_tile_ranges((int64_t)E, ek_s, ts, te, st));
+  // 4. render
+  float *Dm = nullptr, *Wm = nullptr;
+  CK(s->alloc(&Dm, (size_t)std::max<int64_t>(maps, 1)));
+  CK(s->alloc(&Wm, (size_t)std::max<int64_t>(maps, 1)));
+  KL(launch_render(ncam, max_tiles, drc, ts, te, ev_s, rec, Dm, Wm, st));
+  if (J.Dout) TRY(copy_out(s, J.Dout, Dm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
+  if (J.Wout) TRY(copy_out(s, J.Wout, Wm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
+  s->release(ek_s); s->release(ev_s); s->release(ts); s->release(te); s->release(rec); s->release(vals_s);
+  s->release(rcam);
+  // 5. back-projection of every stride-th pixel with weight >= eps_w
+  const uint32_t ns = sp0[ncam];
+  uint32_t *flag = nullptr, *foff = nullptr, *dsp0 = nullptr;
+  CK(s->alloc(&flag, (size_t)ns + 1));
+  CK(s->alloc(&foff, (size_t)ns + 1));
+  CK(s->alloc(&dsp0, (size_t)ncam + 1));
+  CK(cudaMemcpyAsync(dsp0, sp0.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(flag + ns, 0, sizeof(uint32_t), st));
+  KL(launch_bp_count(ncam, max_samples, drc, J.stride, J.eps_w, Wm, dsp0, flag, st));
+  uint64_t np = 0;
+  TRY(scan_counts(s, flag, foff, ns, &np));
+  TRY(grow_cloud(s, J, J.n + (int64_t)np));
+  PrepIn fr{};
+  for (int a = 0; a < 3; ++a) {
+    fr.c0[a] = s->frame.center[a];
+    fr.au[a] = s->frame.axis_u[a];
+    fr.av[a] = s->frame.axis_v[a];
+  }
+  fr.rho = s->frame.radius;
+  KL(launch_bp_write(ncam, max_samples, drc, J.stride, Dm, dsp0, flag, foff, fr, s->mm, (uint32_t)J.n, J.gu, J.gv,
+                     J.cam, st));
+  J.n += (int64_t)np;
+  s->release(flag); s->release(foff); s->release(dsp0); s->release(Dm); s->release(Wm); s->release(drc);
+  return LOBE_OK;
+}
+
 // Load-pass timings and counters (events and pinned counters of the last load).
 void finalize_load_stats(lobe_scene* s) {
   if (!s->stats_pending) return;
@@ -711,7 +897,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -872,6 +1058,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // ---- a2 camera setup (local shard) + camera-centre grid coords
     std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
     std::vector<AnisoCam> haset(std::max<int64_t>(s->N_loc, 1));
+    s->host_cams.assign(cams + s->cam_begin, cams + s->cam_begin + s->N_loc);
     s->cam_gu.assign(s->N_loc, 0.f);
     s->cam_gv.assign(s->N_loc, 0.f);
     for (int64_t c = 0; c < s->N_loc; ++c) {
@@ -1473,6 +1660,119 @@ lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t 
   s->release(dup);
   if (hd != ~0ull) return fail(LOBE_E_INTEGRITY, "origin index " + std::to_string(hd) + " appears twice (SPEC.md:569)");
   return LOBE_OK;
+}
+
+// Shared driver of lobe_render_select / lobe_render_maps.
+lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t cb, int64_t ce, RenderJob& J,
+                           std::vector<uint32_t>* cloud_counts) {
+  if (!coarse || coarse->n != s->G || !coarse->on_device)
+    return fail(LOBE_E_INVALID_CONFIG, "coarse: the loaded Gaussians as device arrays");
+  if (J.ds < 1 || J.stride < 1 || !(J.eps_w >= 0.0f)) return fail(LOBE_E_INVALID_CONFIG, "downscale/stride/eps_w");
+  cudaStream_t st = s->stream;
+  finalize_load_stats(s);
+  SubArgs g{};
+  const float* f[11] = {coarse->x, coarse->y, coarse->z, coarse->sx, coarse->sy, coarse->sz,
+                        coarse->qw, coarse->qx, coarse->qy, coarse->qz, coarse->opacity};
+  for (int k = 0; k < 11; ++k) g.f[k] = f[k];
+  int32_t* perm = nullptr;
+  CK(s->alloc(&perm, (size_t)s->G_pad));
+  KL(launch_perm_from_iperm(s->G, s->iperm, perm, st));
+  const int64_t NL = s->N_loc;
+  std::vector<uint32_t> hoff(NL + 1), hK(std::max<int64_t>(NL, 1));
+  CK(cudaMemcpyAsync(hoff.data(), s->cam_off, sizeof(uint32_t) * (NL + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hK.data(), s->K, sizeof(uint32_t) * std::max<int64_t>(NL, 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<lobe_camera> hcams(s->host_cams.begin(), s->host_cams.end());
+  // batches bounded by the records they hold (the splats of their visible Gaussians)
+  const uint64_t kBudget = 48ull << 20;
+  int64_t c = cb;
+  while (c < ce) {
+    int64_t e = c;
+    uint64_t recs = 0;
+    while (e < ce && (e == c || recs + hK[e] <= kBudget) && e - c < 2048) recs += hK[e++];
+    const int64_t before = J.n;
+    TRY(render_batch(s, g, perm, hoff, hcams, c, e, J));
+    (void)before;
+    c = e;
+  }
+  s->release(perm);
+  if (cloud_counts) {
+    // cloud size per local camera (deterministic integer counts)
+    cloud_counts->assign(std::max<int64_t>(NL, 1), 0);
+    std::vector<uint32_t> hc(J.n);
+    if (J.n > 0) {
+      CK(cudaMemcpyAsync(hc.data(), J.cam, sizeof(uint32_t) * J.n, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    for (uint32_t v : hc) (*cloud_counts)[v] += 1;
+  }
+  CK(cudaStreamSynchronize(st));
+  return LOBE_OK;
+}
+
+lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
+                               float eps_w) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  CK(cudaSetDevice(s->device));
+  RenderJob J;
+  J.ds = downscale <= 0 ? 4 : downscale;
+  J.stride = stride <= 0 ? 2 : stride;
+  J.eps_w = eps_w < 0.0f ? 0.1f : eps_w;
+  std::vector<uint32_t> counts;
+  lobe_status rs = render_cameras(s, coarse, 0, s->N_loc, J, &counts);
+  if (rs != LOBE_OK) {
+    s->release(J.gu); s->release(J.gv); s->release(J.cam);
+    return rs;
+  }
+  s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K);
+  s->cloud_gu = J.gu;
+  s->cloud_gv = J.gv;
+  s->cloud_cam = J.cam;
+  s->n_cloud = J.n;
+  CK(s->alloc(&s->cloud_K, counts.size()));
+  CK(cudaMemcpyAsync(s->cloud_K, counts.data(), sizeof(uint32_t) * counts.size(), cudaMemcpyHostToDevice,
+                     s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->cloud_mode = true;
+  s->ev_valid = false;  // evaluations now count cloud points
+  return LOBE_OK;
+}
+
+lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (!s->cloud_mode) return fail(LOBE_E_STATE, "no clouds: call lobe_render_select first");
+  CK(cudaSetDevice(s->device));
+  const int64_t NL = s->N_loc;
+  std::vector<uint32_t> hk(std::max<int64_t>(NL, 1));
+  CK(cudaMemcpyAsync(hk.data(), s->cloud_K, sizeof(uint32_t) * hk.size(), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (offsets) {
+    offsets[0] = 0;
+    for (int64_t c = 0; c < NL; ++c) offsets[c + 1] = offsets[c] + hk[c];
+  }
+  if (s->n_cloud > capacity) return fail(LOBE_E_CAPACITY, "clouds need " + std::to_string(s->n_cloud));
+  TRY(copy_out(s, gu, s->cloud_gu, sizeof(float) * s->n_cloud));
+  TRY(copy_out(s, gv, s->cloud_gv, sizeof(float) * s->n_cloud));
+  CK(cudaStreamSynchronize(s->stream));
+  return LOBE_OK;
+}
+
+lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
+                             float* depth, float* weight) {
+  g_err.clear();
+  if (!s) return fail(LOBE_E_STATE, "scene is NULL");
+  if (camera < 0 || camera >= s->N_loc) return fail(LOBE_E_INVALID_INDEX, "camera");
+  CK(cudaSetDevice(s->device));
+  RenderJob J;
+  J.ds = downscale <= 0 ? 4 : downscale;
+  J.Dout = depth;
+  J.Wout = weight;
+  lobe_status rs = render_cameras(s, coarse, camera, camera + 1, J, nullptr);
+  s->release(J.gu); s->release(J.gv); s->release(J.cam);
+  CK(cudaStreamSynchronize(s->stream));
+  return rs;
 }
 
 lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* n_cameras, int64_t* n_local_cameras,

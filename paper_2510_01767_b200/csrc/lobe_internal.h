@@ -221,4 +221,42 @@ cudaError_t launch_prune_write(int64_t n, const SubArgs& in, const int64_t* orig
 cudaError_t launch_origin_claim(int64_t n, const int64_t* origin, int64_t G, uint32_t* bits, unsigned long long* dup,
                                 cudaStream_t st);
 
+// ---- NEXT-1 depth-render camera selection (ledger L26) ---------------------
+struct RenderCam {
+  float R[9], t[3];
+  float fx, fy, cx, cy;  // intrinsics at 1/downscale (fp32 divisions, as the oracle)
+  int Wd, Hd, tw, th;    // image and tile-grid size (16 x 16 tiles)
+  uint32_t tile0;        // first tile key of this camera within the batch
+  uint32_t cam;          // local camera index
+  int64_t map0;          // offset of its maps in the batch's D / W buffers
+};
+cudaError_t launch_perm_from_iperm(int64_t G, const int32_t* iperm, int32_t* perm, cudaStream_t st);
+cudaError_t launch_rvis_count(int64_t k0, int64_t nk, const int32_t* cam_order, const uint32_t* pair_tile,
+                              const uint32_t* pair_cam, const uint32_t* rows, int64_t words, uint32_t* cnt,
+                              cudaStream_t st);
+cudaError_t launch_rvis_fill(int64_t k0, int64_t nk, int c0, const int32_t* cam_order, const uint32_t* pair_tile,
+                             const uint32_t* pair_cam, const uint32_t* rows, int64_t words, const uint32_t* pos,
+                             const int32_t* perm, const SubArgs& g, const RenderCam* rc, unsigned long long* keys,
+                             uint32_t* vals, float* rec, uint32_t* rcam, cudaStream_t st);
+cudaError_t seg_sort_u64(void* tmp, size_t& tmp_bytes, const unsigned long long* kin, unsigned long long* kout,
+                         const uint32_t* vin, uint32_t* vout, int64_t n, int nseg, const uint32_t* seg_begin,
+                         const uint32_t* seg_end, cudaStream_t st);
+cudaError_t sort_u32_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
+                           uint32_t* vout, int64_t n, int end_bit, cudaStream_t st);
+cudaError_t launch_bin_count(int64_t n, const uint32_t* svals, const float* rec, const uint32_t* rcam,
+                             const RenderCam* rc, uint32_t* cnt, cudaStream_t st);
+cudaError_t launch_bin_fill(int64_t n, const uint32_t* svals, const float* rec, const uint32_t* rcam,
+                            const RenderCam* rc, const uint32_t* off, uint32_t* ekey, uint32_t* eval, cudaStream_t st);
+cudaError_t launch_tile_ranges(int64_t n, const uint32_t* skey, uint32_t* start, uint32_t* end, cudaStream_t st);
+cudaError_t launch_render(int ncam, int max_tiles, const RenderCam* rc, const uint32_t* start, const uint32_t* end,
+                          const uint32_t* sval, const float* rec, float* Dmap, float* Wmap, cudaStream_t st);
+cudaError_t launch_bp_count(int ncam, int max_samples, const RenderCam* rc, int stride, float eps_w, const float* Wmap,
+                            const uint32_t* sp0, uint32_t* flag, cudaStream_t st);
+cudaError_t launch_bp_write(int ncam, int max_samples, const RenderCam* rc, int stride, const float* Dmap,
+                            const uint32_t* sp0, const uint32_t* flag, const uint32_t* off, const PrepIn& frame,
+                            const float* mm, uint32_t cloud0, float* pgu, float* pgv, uint32_t* pcam,
+                            cudaStream_t st);
+cudaError_t launch_hist_points(int64_t n, const float* pgu, const float* pgv, const uint32_t* pcam,
+                               const ZoneTables* dz, int nzv, int nzp, uint32_t* hist, cudaStream_t st);
+
 }  // namespace lobe

@@ -24,7 +24,8 @@ EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign
            "lobe_crop_masks", "lobe_balance_partition", "lobe_bo_run", "lobe_mask_words", "lobe_block_partial",
            "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
            "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench", "lobe_block_subscene",
-           "lobe_densify_step", "lobe_prune_outside", "lobe_merge_blocks"]
+           "lobe_densify_step", "lobe_prune_outside", "lobe_merge_blocks", "lobe_render_select",
+           "lobe_camera_clouds", "lobe_render_maps"]
 
 
 PREDICATE_ISOTROPIC, PREDICATE_ANISOTROPIC = 0, 1  # lobe_options.predicate (DESIGN.md ledger L24)
@@ -152,6 +153,9 @@ def lib():
                                         SP, i64]
         L.lobe_prune_outside.argtypes = [vp, ctypes.POINTER(Grid), i32, SP, SP, i64]
         L.lobe_merge_blocks.argtypes = [vp, SP, i32, SP, i64]
+        L.lobe_render_select.argtypes = [vp, ctypes.POINTER(Gaussians), i32, i32, ctypes.c_float]
+        L.lobe_camera_clouds.argtypes = [vp, vp, vp, vp, i64]
+        L.lobe_render_maps.argtypes = [vp, ctypes.POINTER(Gaussians), i64, i32, vp, vp]
         L.lobe_masks_combine.argtypes = [vp, i32, vp, i32, vp, vp]
         L.lobe_block_records.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp, vp, vp]
         L.lobe_crop_from_masks.argtypes = [vp, ctypes.POINTER(Grid), vp, vp, vp]
@@ -373,6 +377,35 @@ class Scene:
         so = _sub_struct(d, 0)
         _check(lib().lobe_merge_blocks(self.handle, arr, len(subs), ctypes.byref(so), int(max(tot, 1))))
         return _sub_result(d, so)
+
+    # ---- paper-exact camera selection ---------
+    @staticmethod
+    def _coarse(coarse):
+        arrs = [getattr(coarse, k) for k in SUB_FIELDS]
+        return Gaussians(int(arrs[0].shape[0]), *[_ptr(a) for a in arrs], 1), arrs
+
+    def render_select(self, coarse, downscale=4, stride=2, eps_w=0.1):
+        """Render every local camera's depth, back-project, and assign cameras by
+        their clouds from now on (coarse: the loaded Gaussians, device tensors)."""
+        cg, keep = self._coarse(coarse)
+        _check(lib().lobe_render_select(self.handle, ctypes.byref(cg), int(downscale), int(stride),
+                                        ctypes.c_float(eps_w)))
+
+    def camera_clouds(self):
+        off = np.empty(self.n_local + 1, np.int64)
+        lib().lobe_camera_clouds(self.handle, _ptr(off), None, None, 0)  # size query (offsets are always filled)
+        n = int(off[-1])
+        gu = np.empty(max(n, 1), np.float32)
+        gv = np.empty(max(n, 1), np.float32)
+        _check(lib().lobe_camera_clouds(self.handle, _ptr(off), _ptr(gu), _ptr(gv), max(n, 1)))
+        return off, gu[:n], gv[:n]
+
+    def render_maps(self, coarse, camera, downscale, width, height):
+        cg, keep = self._coarse(coarse)
+        D = np.empty((height // downscale, width // downscale), np.float32)
+        W = np.empty_like(D)
+        _check(lib().lobe_render_maps(self.handle, ctypes.byref(cg), int(camera), int(downscale), _ptr(D), _ptr(W)))
+        return D, W
 
     def export_rows(self, c0=0, count=None):
         count = self.n_local - c0 if count is None else count
