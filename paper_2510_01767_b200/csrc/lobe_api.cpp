@@ -8,6 +8,8 @@
 // -ffp-contract=off: the few fp32 host operations (camera-centre grid
 // coordinates, region bounds) are single IEEE operations in the order written.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
@@ -615,7 +617,38 @@ struct RenderJob {
   int64_t n = 0, cap = 0;
   // optional: maps of the batch's first camera copied here (host or device)
   float *Dout = nullptr, *Wout = nullptr;
+  // grow-only scratch reused by every batch (no pool growth between batches)
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  Buf b[20];
 };
+
+// device scratch slot `k` of at least `bytes` bytes (grow-only)
+template <class T>
+lobe_status scratch(lobe_scene* s, RenderJob& J, int k, T** out, size_t count) {
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  RenderJob::Buf& b = J.b[k];
+  if (b.cap < bytes) {
+    if (b.p) cudaFreeAsync(b.p, s->stream);
+    b.p = nullptr;
+    b.cap = 0;
+    const size_t cap = std::max(bytes, b.cap * 3 / 2);
+    CK(cudaMallocAsync(&b.p, cap, s->stream));
+    b.cap = cap;
+  }
+  *out = static_cast<T*>(b.p);
+  return LOBE_OK;
+}
+void free_scratch(lobe_scene* s, RenderJob& J) {
+  for (auto& b : J.b)
+    if (b.p) {
+      cudaFreeAsync(b.p, s->stream);
+      b.p = nullptr;
+      b.cap = 0;
+    }
+}
 
 lobe_status grow_cloud(lobe_scene* s, RenderJob& J, int64_t need) {
   if (need <= J.cap) return LOBE_OK;
@@ -675,13 +708,13 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
     max_samples = std::max(max_samples, sw * sh);
   }
   RenderCam* drc = nullptr;
-  CK(s->alloc(&drc, (size_t)ncam));
+  TRY(scratch(s, J, 0, &drc, (size_t)ncam));
   CK(cudaMemcpyAsync(drc, rc.data(), sizeof(RenderCam) * ncam, cudaMemcpyHostToDevice, st));
   // 1. records: the visible Gaussians of the batch's non-empty pairs (camera-major)
   const int64_t k0 = hoff[c0], nk = (int64_t)hoff[c1] - k0;
   uint32_t *cnt = nullptr, *pos = nullptr;
-  CK(s->alloc(&cnt, (size_t)nk + 1));
-  CK(s->alloc(&pos, (size_t)nk + 1));
+  TRY(scratch(s, J, 1, &cnt, (size_t)nk + 1));
+  TRY(scratch(s, J, 2, &pos, (size_t)nk + 1));
   CK(cudaMemsetAsync(cnt + nk, 0, sizeof(uint32_t), st));
   KL(launch_rvis_count(k0, nk, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, cnt, st));
   uint64_t n = 0;
@@ -695,11 +728,11 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
   uint32_t *vals = nullptr, *vals_s = nullptr, *rcam = nullptr, *dseg = nullptr;
   float* rec = nullptr;
   const size_t N1 = std::max<uint64_t>(n, 1);
-  CK(s->alloc(&keys, N1)); CK(s->alloc(&keys_s, N1));
-  CK(s->alloc(&vals, N1)); CK(s->alloc(&vals_s, N1));
-  CK(s->alloc(&rcam, N1));
-  CK(s->alloc(&rec, N1 * 10));
-  CK(s->alloc(&dseg, (size_t)ncam + 1));
+  TRY(scratch(s, J, 3, &keys, N1)); TRY(scratch(s, J, 4, &keys_s, N1));
+  TRY(scratch(s, J, 5, &vals, N1)); TRY(scratch(s, J, 6, &vals_s, N1));
+  TRY(scratch(s, J, 7, &rcam, N1));
+  TRY(scratch(s, J, 8, &rec, N1 * 10));
+  TRY(scratch(s, J, 9, &dseg, (size_t)ncam + 1));
   CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
   KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, perm, g, drc,
                       keys, vals, rec, rcam, st));
@@ -707,56 +740,51 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
   if (n > 0) {
     size_t tb = 0;
     CK(seg_sort_u64(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
-    void* tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, tb, st));
+    uint8_t* tmp = nullptr;
+    TRY(scratch(s, J, 10, &tmp, tb));
     CUBL(seg_sort_u64(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
-    cudaFreeAsync(tmp, st);
   }
-  s->release(keys); s->release(keys_s); s->release(vals); s->release(cnt); s->release(pos);
   // 3. tile binning in front-to-back order (stable key sort keeps it)
   uint32_t *c2 = nullptr, *o2 = nullptr;
-  CK(s->alloc(&c2, N1 + 1));
-  CK(s->alloc(&o2, N1 + 1));
+  TRY(scratch(s, J, 1, &c2, N1 + 1));
+  TRY(scratch(s, J, 2, &o2, N1 + 1));
   CK(cudaMemsetAsync(c2 + n, 0, sizeof(uint32_t), st));
   KL(launch_bin_count((int64_t)n, vals_s, rec, rcam, drc, c2, st));
   uint64_t E = 0;
   TRY(scan_counts(s, c2, o2, (int64_t)n, &E));
   uint32_t *ek = nullptr, *ev = nullptr, *ek_s = nullptr, *ev_s = nullptr;
   const size_t E1 = std::max<uint64_t>(E, 1);
-  CK(s->alloc(&ek, E1)); CK(s->alloc(&ev, E1)); CK(s->alloc(&ek_s, E1)); CK(s->alloc(&ev_s, E1));
+  TRY(scratch(s, J, 11, &ek, E1)); TRY(scratch(s, J, 12, &ev, E1));
+  TRY(scratch(s, J, 13, &ek_s, E1)); TRY(scratch(s, J, 14, &ev_s, E1));
   KL(launch_bin_fill((int64_t)n, vals_s, rec, rcam, drc, o2, ek, ev, st));
   int bits = 1;
   while ((1ull << bits) < (unsigned long long)tiles) ++bits;
   if (E > 0) {
     size_t tb = 0;
     CK(sort_u32_pairs(nullptr, tb, ek, ek_s, ev, ev_s, (int64_t)E, bits, st));
-    void* tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, tb, st));
+    uint8_t* tmp = nullptr;
+    TRY(scratch(s, J, 10, &tmp, tb));
     CUBL(sort_u32_pairs(tmp, tb, ek, ek_s, ev, ev_s, (int64_t)E, bits, st));
-    cudaFreeAsync(tmp, st);
   }
-  s->release(ek); s->release(ev); s->release(c2); s->release(o2);
   uint32_t *ts = nullptr, *te = nullptr;
-  CK(s->alloc(&ts, (size_t)tiles + 1));
-  CK(s->alloc(&te, (size_t)tiles + 1));
+  TRY(scratch(s, J, 15, &ts, (size_t)tiles + 1));
+  TRY(scratch(s, J, 16, &te, (size_t)tiles + 1));
   CK(cudaMemsetAsync(ts, 0, sizeof(uint32_t) * (tiles + 1), st));
   CK(cudaMemsetAsync(te, 0, sizeof(uint32_t) * (tiles + 1), st));
   KL(launch_tile_ranges((int64_t)E, ek_s, ts, te, st));
   // 4. render
   float *Dm = nullptr, *Wm = nullptr;
-  CK(s->alloc(&Dm, (size_t)std::max<int64_t>(maps, 1)));
-  CK(s->alloc(&Wm, (size_t)std::max<int64_t>(maps, 1)));
+  TRY(scratch(s, J, 17, &Dm, (size_t)std::max<int64_t>(maps, 1)));
+  TRY(scratch(s, J, 18, &Wm, (size_t)std::max<int64_t>(maps, 1)));
   KL(launch_render(ncam, max_tiles, drc, ts, te, ev_s, rec, Dm, Wm, st));
   if (J.Dout) TRY(copy_out(s, J.Dout, Dm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
   if (J.Wout) TRY(copy_out(s, J.Wout, Wm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
-  s->release(ek_s); s->release(ev_s); s->release(ts); s->release(te); s->release(rec); s->release(vals_s);
-  s->release(rcam);
   // 5. back-projection of every stride-th pixel with weight >= eps_w
   const uint32_t ns = sp0[ncam];
   uint32_t *flag = nullptr, *foff = nullptr, *dsp0 = nullptr;
-  CK(s->alloc(&flag, (size_t)ns + 1));
-  CK(s->alloc(&foff, (size_t)ns + 1));
-  CK(s->alloc(&dsp0, (size_t)ncam + 1));
+  TRY(scratch(s, J, 11, &flag, (size_t)ns + 1));
+  TRY(scratch(s, J, 12, &foff, (size_t)ns + 1));
+  TRY(scratch(s, J, 19, &dsp0, (size_t)ncam + 1));
   CK(cudaMemcpyAsync(dsp0, sp0.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(flag + ns, 0, sizeof(uint32_t), st));
   KL(launch_bp_count(ncam, max_samples, drc, J.stride, J.eps_w, Wm, dsp0, flag, st));
@@ -773,7 +801,6 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
   KL(launch_bp_write(ncam, max_samples, drc, J.stride, Dm, dsp0, flag, foff, fr, s->mm, (uint32_t)J.n, J.gu, J.gv,
                      J.cam, st));
   J.n += (int64_t)np;
-  s->release(flag); s->release(foff); s->release(dsp0); s->release(Dm); s->release(Wm); s->release(drc);
   return LOBE_OK;
 }
 
@@ -1685,26 +1712,34 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
   std::vector<lobe_camera> hcams(s->host_cams.begin(), s->host_cams.end());
   // batches bounded by the records they hold (the splats of their visible Gaussians)
   const uint64_t kBudget = 48ull << 20;
+  const bool trace = std::getenv("LOBE_TRACE") != nullptr;
   int64_t c = cb;
   while (c < ce) {
     int64_t e = c;
     uint64_t recs = 0;
     while (e < ce && (e == c || recs + hK[e] <= kBudget) && e - c < 2048) recs += hK[e++];
-    const int64_t before = J.n;
+    const auto t0 = std::chrono::steady_clock::now();
     TRY(render_batch(s, g, perm, hoff, hcams, c, e, J));
-    (void)before;
+    if (trace) {
+      CK(cudaStreamSynchronize(st));
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      std::fprintf(stderr, "[lobe] render batch cams %lld-%lld records %llu: %.1f ms\n", (long long)c, (long long)e,
+                   (unsigned long long)recs, ms);
+    }
     c = e;
   }
   s->release(perm);
+  free_scratch(s, J);
   if (cloud_counts) {
-    // cloud size per local camera (deterministic integer counts)
+    // cloud size per local camera (integer atomics: order-free)
     cloud_counts->assign(std::max<int64_t>(NL, 1), 0);
-    std::vector<uint32_t> hc(J.n);
-    if (J.n > 0) {
-      CK(cudaMemcpyAsync(hc.data(), J.cam, sizeof(uint32_t) * J.n, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-    }
-    for (uint32_t v : hc) (*cloud_counts)[v] += 1;
+    uint32_t* dc = nullptr;
+    CK(s->alloc(&dc, cloud_counts->size()));
+    CK(cudaMemsetAsync(dc, 0, sizeof(uint32_t) * cloud_counts->size(), st));
+    if (J.n > 0) KL(launch_cam_counts(J.n, J.cam, dc, st));
+    CK(cudaMemcpyAsync(cloud_counts->data(), dc, sizeof(uint32_t) * cloud_counts->size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    s->release(dc);
   }
   CK(cudaStreamSynchronize(st));
   return LOBE_OK;
