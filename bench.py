@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--no-bo", action="store_true")
     p.add_argument("--bo-L", type=int, default=100)
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--render", type=int, default=1, help="also time the depth-render camera selection (NEXT-1)")
     p.add_argument("--predicate", default="iso", choices=["iso", "aniso"],
                    help="visibility predicate: iso = SPEC.md:299 bound (the metric's path), aniso = EWA footprint")
     return p.parse_args()
@@ -326,6 +327,22 @@ def main():
               "objective_uniform": int(r["history"][0]), "objective_best": int(r["history"].min()),
               "improvement": 1.0 - float(r["history"].min()) / max(1, int(r["history"][0])),
               "tests_executed": int(st.tests_executed)}
+        # paper-exact camera selection (ledger L26): depth
+        # render + back-projection of every camera, then the BO loop on the clouds
+        if args.render and world == 1:
+            barrier()
+            t0 = time.perf_counter()
+            eng.local.render_select(dg)
+            barrier()
+            rs = time.perf_counter() - t0
+            off, _, _ = eng.local.camera_clouds()
+            t0 = time.perf_counter()
+            r2 = eng.balance_partition(m, n, L=args.bo_L, seed=0)
+            bo2 = time.perf_counter() - t0
+            bo["render_selection"] = {"seconds": rs, "cameras": int(N), "cloud_points": int(off[-1]),
+                                      "downscale": 4, "stride": 2, "eps_w": 0.1,
+                                      "bo_seconds": bo2, "objective_uniform": int(r2["history"][0]),
+                                      "objective_best": int(r2["history"].min())}
         eng.close()
 
     if rank != 0:
