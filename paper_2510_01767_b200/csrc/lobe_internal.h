@@ -75,8 +75,9 @@ cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, u
 cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, const float* x,
                              const float* y, const float* z, const float* kk, const float* o, float4* rec,
                              cudaStream_t st);
+// stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit)
 cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
-                             int32_t* vout, int64_t n, cudaStream_t st);
+                             int32_t* vout, int64_t n, cudaStream_t st, int begin_bit = 0, int end_bit = 32);
 // Gather into the internal pair-interleaved layout, build the inverse permutation;
 // anisotropic: also Sigma, cv[3 (32 g + l) + {0,1,2}] = {S00A,S00B,S01A,S01B},
 // {S02A,S02B,S11A,S11B}, {S12A,S12B,S22A,S22B}.
