@@ -1063,10 +1063,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
     KL(launch_prep_norm(G, ru, rv, s->mm, din[0], din[1], din[2], kk, din[10], rec, st));
     size_t tmpb = 0;
-    CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 0, 30));  // 30-bit Morton keys
+    CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));  // top 24 of the 30-bit Morton keys
     void* tmp = nullptr;
     CK(cudaMallocAsync(&tmp, tmpb, st));
-    CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st, 0, 30));
+    CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));
     CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->o2, (size_t)s->G_pad));
