@@ -251,6 +251,7 @@ def main():
         stats_acc["dense"] = st.dense_tests
         stats_acc["kept"] = st.kept_tests
         stats_acc["accepted"] = st.accepted_tests
+        stats_acc["variants"] = list(st.exact_variant_tests)
         stats_acc["kernels"] += st.kernel_launches
         stats_acc["cub"] += st.cub_launches
         stats_acc["tests"] += st.tests_executed
@@ -384,6 +385,8 @@ def main():
             "decided_by_bounds": {"tile_rejected": int(G * n_local - kept_tests),
                                   "slice_rejected": int(kept_tests - dense_tests - accepted_tests),
                                   "slice_accepted": int(accepted_tests)},
+            "exact_tests_by_open_conditions": dict(zip(("left_edge", "top_edge", "right_edge", "bottom_edge",
+                                                        "four_edges", "all_six"), stats_acc.get("variants", []))),
             "logical_tests_per_s_kernel": G * n_local / (t_vis * 1e-3),
             "executed_tests_per_s_kernel": dense_tests / (t_vis * 1e-3),
             "depth_stat_ms": t_depth,

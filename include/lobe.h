@@ -181,6 +181,8 @@ typedef struct {
   uint64_t cub_launches;    /* cumulative CUB primitive calls (radix sort, scan) */
   uint64_t kept_tests;      /* tests in (tile, camera) pairs the tile bound did not reject (last pass) */
   uint64_t accepted_tests;  /* tests in (slice, camera) pairs the slice bound accepted (last pass) */
+  uint64_t exact_variant_tests[6]; /* exact tests by the conditions left open: left edge only, top edge only,
+                                      right edge only, bottom edge only, the four edges, all six */
 } lobe_stats;
 
 /* ---- scene --------------------------------------------------------------- */

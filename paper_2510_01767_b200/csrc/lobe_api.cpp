@@ -160,7 +160,7 @@ struct lobe_scene {
     uint8_t zp_cell[kMaxZones * kMaxZones];
     alignas(16) uint32_t counts[3 * kMaxBlocks];  // mirrors the device block: ncams, gvis, gblk
     unsigned long long incid[kMaxBlocks];   // then incid (contiguous on the device too)
-    unsigned long long vc[2];               // k_vis_tiles counters of the last pass
+    unsigned long long vc[8];               // k_vis_tiles counters of the last pass
   };
   static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
                 "pinned counts / incid must mirror the contiguous device block");
@@ -816,6 +816,7 @@ void finalize_load_stats(lobe_scene* s) {
   s->st.kept_tests = (uint64_t)s->kept_pairs_last * (uint64_t)kTile;  // pairs surviving the tile bound
   s->st.dense_tests = (uint64_t)s->pin->vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
   s->st.accepted_tests = (uint64_t)s->pin->vc[1] * (uint64_t)(kTile / 4);
+  for (int v = 0; v < 6; ++v) s->st.exact_variant_tests[v] = (uint64_t)s->pin->vc[2 + v] * (uint64_t)(kTile / 4);
   s->stats_pending = false;
 }
 
@@ -1115,7 +1116,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
     CK(s->alloc(&s->slice_lo, (size_t)s->n_tiles * 4));
     CK(s->alloc(&s->slice_hi, (size_t)s->n_tiles * 4));
-    CK(s->alloc(&s->vcnt, 2));
+    CK(s->alloc(&s->vcnt, 8));
     CK(s->alloc(&s->chunk_lo, (size_t)s->n_chunks));
     CK(s->alloc(&s->chunk_hi, (size_t)s->n_chunks));
     CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
@@ -1179,7 +1180,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     s->release(uc);
     s->release(uoff);
-    CK(cudaMemsetAsync(s->vcnt, 0, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(s->vcnt, 0, 8 * sizeof(unsigned long long), st));
     CK(cudaEventRecord(s->ev[9], st));
     if (s->N_loc > 0 && kept_pairs > 0) {
       VisArgs va{};

@@ -114,7 +114,7 @@ class Stats(ctypes.Structure):
                 ("t_depth_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_uint64),
                 ("cub_launches", ctypes.c_uint64), ("kept_tests", ctypes.c_uint64),
-                ("accepted_tests", ctypes.c_uint64)]
+                ("accepted_tests", ctypes.c_uint64), ("exact_variant_tests", ctypes.c_uint64 * 6)]
 
 
 OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
