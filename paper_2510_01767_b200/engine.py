@@ -110,6 +110,12 @@ class Engine:
             self.block_loads(m, n, **grid_kw)
         return self.local.crop_from_masks_into(m, n, self._comb, crop_out, elig_out, **grid_kw)
 
+    def render_select(self, coarse, downscale=4, stride=2, eps_w=0.1):
+        """Paper-exact camera selection: every rank renders its
+        own cameras; assignments stay per camera, so the exchange is unchanged."""
+        self.local.render_select(coarse, downscale=downscale, stride=stride, eps_w=eps_w)
+        self._comb_key = None
+
     def close(self):
         self._comb = None
         if hasattr(self.local, "close"):
