@@ -218,7 +218,9 @@ lobe_status lobe_block_loads(lobe_scene* scene, const lobe_grid* grid, lobe_bloc
 /* crop, eligible: B x ceil(G/64) u64, caller order. crop_b = union of the rows
  * of C^(b) (visibility cropping); eligible_b = crop_b and
  * "centre in the delta = 0 cell of b" (selective densification).
- * Either may be NULL. */
+ * Either may be NULL. Host outputs are complete on return; device outputs (on
+ * the scene's device) are written in the order of the scene's stream -- the
+ * call returns without waiting, like a kernel launch. */
 lobe_status lobe_crop_masks(lobe_scene* scene, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible);
 
 /* Load-balanced cuts: uniform cuts first, then n_sobol

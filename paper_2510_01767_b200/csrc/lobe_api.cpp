@@ -168,6 +168,7 @@ struct lobe_scene {
   uint8_t* pin_out = nullptr;  // growable staging for per-camera outputs
   size_t pin_out_cap = 0;
   bool stats_pending = false;  // load-pass timings read lazily (lobe_get_stats)
+  bool crop_pending = false;   // crop timing of a call with device outputs, read lazily
   unsigned long long kept_pairs_last = 0;
   const uint32_t* h_ncams() const { return pin->counts; }
   const uint32_t* h_gvis() const { return pin->counts + kMaxBlocks; }
@@ -175,7 +176,7 @@ struct lobe_scene {
   const unsigned long long* h_incid() const { return pin->incid; }
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[14] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4; crop / comm: 5, 6; dev bench: 6, 7
+  cudaEvent_t ev[16] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -1407,9 +1408,9 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   uint8_t* cb8 = nullptr;
   CK(s->alloc(&mbits, (size_t)s->words * 32));
   CK(s->alloc(&cb8, (size_t)s->words * 32));
-  CK(cudaEventRecord(s->ev[5], s->stream));
+  CK(cudaEventRecord(s->ev[14], s->stream));
   KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream));
-  CK(cudaEventRecord(s->ev[6], s->stream));
+  CK(cudaEventRecord(s->ev[15], s->stream));
   if (crop && !crop_dev) {
     TRY(copy_out(s, crop, dc, bytes));
     s->release(dc);
@@ -1420,8 +1421,12 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   }
   s->release(mbits);
   s->release(cb8);
-  CK(cudaStreamSynchronize(s->stream));
-  s->st.t_crop_ms = ms_between(s->ev[5], s->ev[6]);
+  if ((crop && !crop_dev) || (eligible && !elig_dev)) {
+    CK(cudaStreamSynchronize(s->stream));  // host outputs are complete on return
+    s->st.t_crop_ms = ms_between(s->ev[14], s->ev[15]);
+  } else {
+    s->crop_pending = true;  // device outputs: stream-ordered; timing read lazily
+  }
   return LOBE_OK;
 }
 
@@ -1826,6 +1831,12 @@ lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* 
 lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
   finalize_load_stats(const_cast<lobe_scene*>(s));
+  if (s->crop_pending) {
+    lobe_scene* w = const_cast<lobe_scene*>(s);
+    cudaEventSynchronize(w->ev[15]);
+    w->st.t_crop_ms = ms_between(w->ev[14], w->ev[15]);
+    w->crop_pending = false;
+  }
   *out = s->st;
   return LOBE_OK;
 }
