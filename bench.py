@@ -388,7 +388,7 @@ def main():
                                   "slice_rejected": int(kept_tests - dense_tests - accepted_tests),
                                   "slice_accepted": int(accepted_tests)},
             "exact_tests_by_open_conditions": dict(zip(("left_edge", "top_edge", "right_edge", "bottom_edge",
-                                                        "four_edges", "all_six"), stats_acc.get("variants", []))),
+                                                        "two_or_four_edges", "all_six"), stats_acc.get("variants", []))),
             "logical_tests_per_s_kernel": G * n_local / (t_vis * 1e-3),
             "executed_tests_per_s_kernel": dense_tests / (t_vis * 1e-3),
             "depth_stat_ms": t_depth,
