@@ -737,13 +737,17 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
   CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
   KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, perm, g, drc,
                       keys, vals, rec, rcam, st));
-  // 2. front to back per camera: (zc, caller index)
+  // 2. front to back per camera: (zc, caller index) -- one radix sort on
+  //    (camera, zc bits), then runs of equal depth ordered by caller index
   if (n > 0) {
+    int cb = 1;
+    while ((1 << cb) < ncam) ++cb;
     size_t tb = 0;
-    CK(seg_sort_u64(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
+    CK(sort_u64_pairs(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, 32 + cb, st));
     uint8_t* tmp = nullptr;
     TRY(scratch(s, J, 10, &tmp, tb));
-    CUBL(seg_sort_u64(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, ncam, dseg, dseg + 1, st));
+    CUBL(sort_u64_pairs(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, 32 + cb, st));
+    KL(launch_tie_fix((int64_t)n, keys_s, vals_s, rec, st));
   }
   // 3. tile binning in front-to-back order (stable key sort keeps it)
   uint32_t *c2 = nullptr, *o2 = nullptr;

@@ -242,6 +242,9 @@ cudaError_t launch_rvis_fill(int64_t k0, int64_t nk, int c0, const int32_t* cam_
 cudaError_t seg_sort_u64(void* tmp, size_t& tmp_bytes, const unsigned long long* kin, unsigned long long* kout,
                          const uint32_t* vin, uint32_t* vout, int64_t n, int nseg, const uint32_t* seg_begin,
                          const uint32_t* seg_end, cudaStream_t st);
+cudaError_t sort_u64_pairs(void* tmp, size_t& tmp_bytes, const unsigned long long* kin, unsigned long long* kout,
+                           const uint32_t* vin, uint32_t* vout, int64_t n, int end_bit, cudaStream_t st);
+cudaError_t launch_tie_fix(int64_t n, const unsigned long long* key, uint32_t* val, const float* rec, cudaStream_t st);
 cudaError_t sort_u32_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
                            uint32_t* vout, int64_t n, int end_bit, cudaStream_t st);
 cudaError_t launch_bin_count(int64_t n, const uint32_t* svals, const float* rec, const uint32_t* rcam,
