@@ -226,7 +226,7 @@ def test_bo_trajectory_parity_and_I16():
         assert st.tests_executed == sc.G * sc.N and st.vis_launches == 1
 
 
-@pytest.mark.parametrize("name", ["rubble", "matrixcity"])
+@pytest.mark.parametrize("name", ["rubble", "building", "residence", "matrixcity"])
 def test_full_size_sampled(name):
     """BASELINE configs at full size, in the launch configuration bench.py times:
     rows / per-camera outputs bit-exact on sampled cameras (the oracle computes
@@ -442,3 +442,23 @@ def test_aniso_fuzz_culling_exact(seed, G):
 def test_aniso_edge_clusters_exact(seed):
     st = full_parity(_edge_scene(seed), [oracle.default_grid(2, 2)], predicate=1)
     assert st.dense_tests > 0
+
+
+def test_full_size_sampled_aniso():
+    """The anisotropic mode at MatrixCity size: rows and per-camera outputs of
+    sampled cameras equal the oracle's O6a."""
+    lobe = _lobe()
+    sc = make_scene("matrixcity")
+    m, n = sc.cfg.m, sc.cfg.n
+    rng = np.random.default_rng(23)
+    sel = np.sort(rng.choice(sc.N, 4, replace=False))
+    with lobe.Scene(sc, sc, predicate=1) as S:
+        fr = oracle.frame(sc)
+        pre = oracle.prep(sc, fr)
+        pre["cam_gu_sel"], pre["cam_gv_sel"] = pre["cam_gu"][sel], pre["cam_gv"][sel]
+        vis = oracle.visibility_aniso(sc, pre, cams=sel)
+        rows = np.concatenate([S.export_rows(int(c), 1) for c in sel])
+        assert (rows == vis["rows"]).all()
+        g = oracle.default_grid(m, n)
+        asg = oracle.assign(sc, pre, vis, g)
+        _cmp_percam(S.assign_cameras(m, n), vis, asg, sel=sel)
