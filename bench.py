@@ -241,10 +241,11 @@ def main():
 
     def step(gsrc, crop_out, elig_out):
         eng = Engine.from_scene(gsrc, cams, stream=stream, group=group, predicate=pred)
-        L = eng.block_loads(m, n)
-        # device crop outputs are stream-ordered: the crop runs while the host
-        # prepares the per-camera outputs; assign_cameras' copy waits for it
+        # nothing here waits for the device until block_loads reads the block
+        # counts: the evaluation and the crop are enqueued first, so the crop
+        # runs while the host builds the records; assign_cameras' copies follow
         eng.crop_masks_into(m, n, crop_out, elig_out)
+        L = eng.block_loads(m, n)
         A = eng.assign_cameras(m, n)
         st = eng.local.stats()
         stats_acc["t_vis_ms"].append(st.t_vis_ms)

@@ -94,7 +94,6 @@ struct lobe_scene {
   int64_t words = 0, n_tiles = 0, n_chunks = 0;
   lobe_frame frame{};
   float mm[4] = {0, 0, 0, 0};
-  std::vector<float> cam_gu, cam_gv;
   // device, internal order
   float *xy = nullptr, *zk = nullptr, *o2 = nullptr, *gu = nullptr, *gv = nullptr;
   int32_t* iperm = nullptr;
@@ -161,6 +160,8 @@ struct lobe_scene {
     alignas(16) uint32_t counts[3 * kMaxBlocks];  // mirrors the device block: ncams, gvis, gblk
     unsigned long long incid[kMaxBlocks];   // then incid (contiguous on the device too)
     unsigned long long vc[8];               // k_vis_tiles counters of the last pass
+    uint32_t prep_hs[8];                    // k_prep_raw: error flags, ordered ground min / max
+    unsigned long long prep_bad;            // k_prep_raw: first invalid Gaussian
   };
   static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
                 "pinned counts / incid must mirror the contiguous device block");
@@ -170,13 +171,24 @@ struct lobe_scene {
   bool stats_pending = false;  // load-pass timings read lazily (lobe_get_stats)
   bool crop_pending = false;   // crop timing of a call with device outputs, read lazily
   unsigned long long kept_pairs_last = 0;
-  const uint32_t* h_ncams() const { return pin->counts; }
-  const uint32_t* h_gvis() const { return pin->counts + kMaxBlocks; }
-  const uint32_t* h_gblk() const { return pin->counts + 2 * kMaxBlocks; }
-  const unsigned long long* h_incid() const { return pin->incid; }
+  // An evaluation ends with an asynchronous copy of its block counts into
+  // `pin` (event ev[13]); the host waits only when it reads them.
+  bool eval_pending = false;
+  void wait_counts() {
+    if (!eval_pending) return;
+    cudaEventSynchronize(ev[13]);
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, ev[2], ev[3]) == cudaSuccess) st.t_hist_ms = a;
+    if (cudaEventElapsedTime(&b, ev[3], ev[4]) == cudaSuccess) st.t_loads_ms = b;
+    eval_pending = false;
+  }
+  const uint32_t* h_ncams() { wait_counts(); return pin->counts; }
+  const uint32_t* h_gvis() { wait_counts(); return pin->counts + kMaxBlocks; }
+  const uint32_t* h_gblk() { wait_counts(); return pin->counts + 2 * kMaxBlocks; }
+  const unsigned long long* h_incid() { wait_counts(); return pin->incid; }
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[16] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
+  cudaEvent_t ev[16] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4, 13; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -415,6 +427,7 @@ float ms_between(cudaEvent_t a, cudaEvent_t b) {
 // a5 + a6 + a7 (+ a8 into `masks_out`): one evaluation of a grid on cached rows.
 lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   cudaStream_t st = s->stream;
+  s->wait_counts();  // the previous evaluation's copies read / write `pin`
   // ---- a5 zone tables (host) + per-Gaussian zones (device)
   ZoneTables Z{};
   build_axis(g.m, g.v, g.dv, &Z.U);
@@ -477,9 +490,8 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   CK(cudaMemcpyAsync(s->pin->counts, s->counts,
                      sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks,
                      cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  s->st.t_hist_ms = ms_between(s->ev[2], s->ev[3]);
-  s->st.t_loads_ms = ms_between(s->ev[3], s->ev[4]);
+  CK(cudaEventRecord(s->ev[13], st));
+  s->eval_pending = true;  // no synchronisation: readers of the counts wait (wait_counts)
   s->st.evaluations += 1;
   return LOBE_OK;
 }
@@ -507,7 +519,7 @@ lobe_status ensure_eval(lobe_scene* s, const GridV& g) {
   return LOBE_OK;
 }
 
-void fill_records(const lobe_scene* s, const GridV& g, const uint32_t* ncams, const uint64_t* incid,
+void fill_records(lobe_scene* s, const GridV& g, const uint32_t* ncams, const uint64_t* incid,
                   const uint32_t* gvis, lobe_block_load* out, uint32_t* objective) {
   std::vector<float> ulo(g.m), uhi(g.m), uelo(g.m), uehi(g.m), vlo(g.n), vhi(g.n), velo(g.n), vehi(g.n);
   for (int p = 0; p < g.m; ++p) {
@@ -1048,26 +1060,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     pin.rho = F.radius;
     pin.cov = cov_raw;
     KL(launch_prep_raw(pin, ru, rv, kk, keys, vals, scratch, err_idx, scratch + 1, st));
-    uint32_t hs[8];
-    unsigned long long hbad;
-    CK(cudaMemcpyAsync(hs, scratch, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hbad, err_idx, sizeof(hbad), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hs[0] & 1u)
-      return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(hbad) +
-                                            " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
-                                            "SPEC.md:30-33)");
-    if (hs[0] & 2u) return fail(LOBE_E_INVALID_INPUT, "non-finite grid coordinate at " + std::to_string(hbad));
-    auto ord2f = [](uint32_t u) {
-      uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-      float f;
-      std::memcpy(&f, &b, 4);
-      return f;
-    };
-    s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
-    if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
-      return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
-    KL(launch_prep_norm(G, ru, rv, s->mm, din[0], din[1], din[2], kk, din[10], rec, st));
+    // validation flags and the ground min / max reach the host asynchronously;
+    // they are checked at the first synchronisation (after the culling pass)
+    CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), cudaMemcpyDeviceToHost, st));
+    KL(launch_prep_norm(G, ru, rv, scratch + 1, din[0], din[1], din[2], kk, din[10], rec, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));  // top 24 of the 30-bit Morton keys
     void* tmp = nullptr;
@@ -1084,7 +1081,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->release(cov_raw);
     cudaFreeAsync(tmp, st);
     s->release(ru); s->release(rv); s->release(kk); s->release(rec);
-    s->release(keys); s->release(keys_s); s->release(vals); s->release(perm); s->release(scratch);
+    s->release(keys); s->release(keys_s); s->release(vals); s->release(perm);
     s->release(err_idx);
     if (dev_in) s->release(dev_in);
 
@@ -1092,20 +1089,14 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     std::vector<CamSetup> hset(std::max<int64_t>(s->N_loc, 1));
     std::vector<AnisoCam> haset(std::max<int64_t>(s->N_loc, 1));
     s->host_cams.assign(cams + s->cam_begin, cams + s->cam_begin + s->N_loc);
-    s->cam_gu.assign(s->N_loc, 0.f);
-    s->cam_gv.assign(s->N_loc, 0.f);
-    for (int64_t c = 0; c < s->N_loc; ++c) {
+    std::vector<float> cam_ru(std::max<int64_t>(s->N_loc, 1)), cam_rv(std::max<int64_t>(s->N_loc, 1));
+    for (int64_t c = 0; c < s->N_loc; ++c) {  // host work overlapping the device's a1 pass
       const lobe_camera& k = cams[s->cam_begin + c];
       hset[c] = camera_setup(k);
       if (s->aniso) haset[c] = aniso_setup(k);
       double oc[3];
       cam_centre(k, oc);
-      float ru_, rv_;
-      ground_uv_host((float)oc[0], (float)oc[1], (float)oc[2], F, &ru_, &rv_);
-      float a = (ru_ - s->mm[0]) / (s->mm[1] - s->mm[0]);
-      float b = (rv_ - s->mm[2]) / (s->mm[3] - s->mm[2]);
-      s->cam_gu[c] = std::fmin(1.0f, std::fmax(0.0f, a));
-      s->cam_gv[c] = std::fmin(1.0f, std::fmax(0.0f, b));
+      ground_uv_host((float)oc[0], (float)oc[1], (float)oc[2], F, &cam_ru[c], &cam_rv[c]);
     }
     const int64_t NL = std::max<int64_t>(s->N_loc, 1);
     CK(s->alloc(&s->cams, NL));
@@ -1115,6 +1106,15 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     if (s->aniso) {
       CK(s->alloc(&s->acams, NL));
       CK(cudaMemcpyAsync(s->acams, haset.data(), sizeof(AnisoCam) * NL, cudaMemcpyHostToDevice, st));
+    }
+    {  // camera-centre grid coordinates, normalised on the device with k_prep_raw's min / max
+      float* cr;
+      CK(s->alloc(&cr, (size_t)2 * NL));
+      CK(cudaMemcpyAsync(cr, cam_ru.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(cr + NL, cam_rv.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, st));
+      if (s->N_loc > 0) KL(launch_cam_grid(s->N_loc, cr, cr + NL, scratch + 1, s->d_cam_gu, s->d_cam_gv, st));
+      s->release(cr);
+      s->release(scratch);
     }
     s->n_sub = (NL + 31) / 32;
     CK(s->alloc(&s->tile_lo, (size_t)s->n_tiles));
@@ -1128,10 +1128,6 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->kept, 1));
     KL(launch_tile_bounds(reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk), s->n_tiles,
                           s->tile_lo, s->tile_hi, s->slice_lo, s->slice_hi, st));
-    if (s->N_loc > 0) {
-      CK(cudaMemcpyAsync(s->d_cam_gu, s->cam_gu.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(s->d_cam_gv, s->cam_gv.data(), sizeof(float) * s->N_loc, cudaMemcpyHostToDevice, st));
-    }
     // ---- a3/a4 visibility pass
     CK(s->alloc(&s->rows, (size_t)NL * s->words));
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
@@ -1174,6 +1170,24 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(cudaMemcpyAsync(&nu, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     s->n_units = nu;
+    {  // k_prep_raw's verdict (its copies completed with this synchronisation)
+      const uint32_t* hs = s->pin->prep_hs;
+      const unsigned long long hbad = s->pin->prep_bad;
+      if (hs[0] & 1u)
+        return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(hbad) +
+                                              " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
+                                              "SPEC.md:30-33)");
+      if (hs[0] & 2u) return fail(LOBE_E_INVALID_INPUT, "non-finite grid coordinate at " + std::to_string(hbad));
+      auto ord2f = [](uint32_t u) {
+        uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+        float f;
+        std::memcpy(&f, &b, 4);
+        return f;
+      };
+      s->mm[0] = ord2f(hs[1]); s->mm[1] = ord2f(hs[2]); s->mm[2] = ord2f(hs[3]); s->mm[3] = ord2f(hs[4]);
+      if (s->mm[1] == s->mm[0] || s->mm[3] == s->mm[2])
+        return fail(LOBE_E_DEGENERATE_SCENE, "all Gaussians share a ground coordinate (SPEC.md:80)");
+    }
     CK(s->alloc(&s->klist, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(s->alloc(&s->nonempty, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
@@ -1835,6 +1849,7 @@ lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* 
 lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
   finalize_load_stats(const_cast<lobe_scene*>(s));
+  const_cast<lobe_scene*>(s)->wait_counts();
   if (s->crop_pending) {
     lobe_scene* w = const_cast<lobe_scene*>(s);
     cudaEventSynchronize(w->ev[15]);

@@ -72,7 +72,9 @@ static_assert(sizeof(AnisoCam) == 96, "AnisoCam layout");
 cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* keys, int32_t* vals,
                             uint32_t* err, unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
 // Normalise the ground coordinates to [0,1].
-cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const float* mm, const float* x,
+cudaError_t launch_cam_grid(int64_t N, const float* ru, const float* rv, const uint32_t* mm_ord, float* gu, float* gv,
+                            cudaStream_t st);
+cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const uint32_t* mm_ord, const float* x,
                              const float* y, const float* z, const float* kk, const float* o, float4* rec,
                              cudaStream_t st);
 // stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit)

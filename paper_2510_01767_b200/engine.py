@@ -48,6 +48,7 @@ class Engine:
         self.device = getattr(local, "device", None) or ("cuda" if torch.cuda.is_available() else "cpu")
         self._comb_key = None
         self._comb = None
+        self._loads = None
 
     @classmethod
     def from_scene(cls, gaussians, cameras, frame=None, device=None, stream=None, assign_mode=0, group=None,
@@ -80,6 +81,9 @@ class Engine:
     def block_loads(self, m, n, **grid_kw):
         if self.world == 1:
             return self.local.block_loads(m, n, **grid_kw)
+        key = self._grid_key(m, n, grid_kw)
+        if self._comb_key == key and self._loads is not None:
+            return self._loads  # this grid was already exchanged (e.g. by crop_masks first)
         B = m * n
         words = self.local.mask_words()
         part = torch.zeros(B * words, dtype=torch.int32, device=self.device)
@@ -90,10 +94,11 @@ class Engine:
         counts = torch.from_numpy(np.concatenate([nc.astype(np.int64), inc.astype(np.int64)])).to(self.device)
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
         counts = counts.cpu().numpy()
-        self._comb_key = self._grid_key(m, n, grid_kw)
+        self._comb_key = key
         self._comb = comb
-        return self.local.block_records(m, n, counts[:B].astype(np.uint32), counts[B:].astype(np.uint64), gv,
-                                        **grid_kw)
+        self._loads = self.local.block_records(m, n, counts[:B].astype(np.uint32), counts[B:].astype(np.uint64),
+                                               gv, **grid_kw)
+        return self._loads
 
     def crop_masks(self, m, n, **grid_kw):
         if self.world == 1:
@@ -115,9 +120,11 @@ class Engine:
         own cameras; assignments stay per camera, so the exchange is unchanged."""
         self.local.render_select(coarse, downscale=downscale, stride=stride, eps_w=eps_w)
         self._comb_key = None
+        self._loads = None
 
     def close(self):
         self._comb = None
+        self._loads = None
         if hasattr(self.local, "close"):
             self.local.close()
 

@@ -25,8 +25,8 @@ stream = torch.cuda.current_stream()
 
 def step():
     eng = Engine.from_scene(dg, cams, stream=stream)
-    eng.block_loads(m, n)
     eng.crop_masks_into(m, n, crop, elig)
+    eng.block_loads(m, n)
     eng.assign_cameras(m, n)
     eng.close()
 
