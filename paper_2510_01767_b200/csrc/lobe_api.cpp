@@ -161,6 +161,7 @@ struct lobe_scene {
     unsigned long long incid[kMaxBlocks];   // then incid (contiguous on the device too)
     unsigned long long vc[8];               // k_vis_tiles counters of the last pass
     uint32_t prep_hs[8];                    // k_prep_raw: error flags, ordered ground min / max
+    uint32_t n_pairs;                       // non-empty (tile, camera) pairs of the last load
     unsigned long long prep_bad;            // k_prep_raw: first invalid Gaussian
   };
   static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
@@ -830,6 +831,8 @@ void finalize_load_stats(lobe_scene* s) {
   s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
   s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
   s->st.t_depth_ms = ms_between(s->ev[11], s->ev[12]);
+  s->n_pairs = s->pin->n_pairs;
+  s->st.tile_pairs = (uint64_t)s->n_pairs;
   s->st.kept_tests = (uint64_t)s->kept_pairs_last * (uint64_t)kTile;  // pairs surviving the tile bound
   s->st.dense_tests = (uint64_t)s->pin->vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
   s->st.accepted_tests = (uint64_t)s->pin->vc[1] * (uint64_t)(kTile / 4);
@@ -1239,27 +1242,35 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CUBL(exclusive_scan_u32(tmp, sb, cnt, s->tile_off, s->n_tiles + 1, st));
     cudaFreeAsync(tmp, st);
     s->release(cnt);
-    uint32_t np = 0;
-    CK(cudaMemcpyAsync(&np, s->tile_off + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    s->n_pairs = np;
-    CK(s->alloc(&s->pair_cam, (size_t)np));
-    CK(s->alloc(&s->pair_tile, (size_t)np));
-    if (s->N_loc > 0 && np > 0)
-      KL(launch_tile_fill(s->koff, s->klist, s->nonempty, s->n_tiles, s->tile_off, s->pair_cam, s->pair_tile, st));
+    // the pair count stays on the device: lists are sized by the kept pairs
+    // (an upper bound known since the culling pass); the host reads the count
+    // lazily with the statistics
+    CK(cudaMemcpyAsync(&s->pin->n_pairs, s->tile_off + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    const int64_t cap = (int64_t)std::max<unsigned long long>(kept_pairs, 1);
+    const int64_t tw = (s->n_tiles + 31) / 32;
+    CK(s->alloc(&s->pair_cam, (size_t)cap));
+    CK(s->alloc(&s->pair_tile, (size_t)cap));
+    uint32_t *camtile = nullptr, *wordpre = nullptr;
+    CK(s->alloc(&camtile, (size_t)NL * tw));
+    CK(cudaMemsetAsync(camtile, 0, sizeof(uint32_t) * NL * tw, st));
+    if (s->N_loc > 0 && kept_pairs > 0)
+      KL(launch_tile_fill(s->koff, s->klist, s->nonempty, s->n_tiles, s->tile_off, s->pair_cam, s->pair_tile,
+                          camtile, tw, st));
     // ---- a4 depth statistic over the non-empty (tile, camera) pairs
     CK(cudaEventRecord(s->ev[11], st));
-    CK(s->alloc(&s->pair_part, (size_t)std::max<int64_t>(np, 1)));
+    CK(s->alloc(&s->pair_part, (size_t)cap));
     CK(s->alloc(&s->cam_off, (size_t)NL + 1));
-    CK(s->alloc(&s->cam_order, (size_t)std::max<int64_t>(np, 1)));
+    CK(s->alloc(&s->cam_order, (size_t)cap));
     if (s->N_loc > 0) {
       KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, reinterpret_cast<const float4*>(s->xy),
                             reinterpret_cast<const float4*>(s->zk), reinterpret_cast<const float2*>(s->o2), s->cams,
                             s->pair_part, st));
+      // pair indices in camera-major order, tile order within a camera
       uint32_t* ccount;
       CK(s->alloc(&ccount, (size_t)NL + 1));
-      CK(cudaMemsetAsync(ccount, 0, sizeof(uint32_t) * (NL + 1), st));
-      KL(launch_cam_counts(np, s->pair_cam, ccount, st));
+      CK(s->alloc(&wordpre, (size_t)NL * tw));
+      CK(cudaMemsetAsync(ccount + NL, 0, sizeof(uint32_t), st));
+      KL(launch_cam_order(s->N_loc, tw, camtile, wordpre, ccount, st));
       size_t sb2 = 0;
       CK(exclusive_scan_u32(nullptr, sb2, ccount, s->cam_off, NL + 1, st));
       void* tmp2 = nullptr;
@@ -1267,25 +1278,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
       cudaFreeAsync(tmp2, st);
       s->release(ccount);
-      if (np > 0) {  // pair indices ordered by camera, tile order kept (stable)
-        uint32_t* ksorted;
-        int32_t* iota;
-        CK(s->alloc(&ksorted, (size_t)np));
-        CK(s->alloc(&iota, (size_t)np));
-        KL(launch_iota(iota, np, st));
-        size_t sb3 = 0;
-        int cbits = 1;
-        while ((1ll << cbits) < NL) ++cbits;  // camera ids < N_local
-        CK(radix_sort_pairs(nullptr, sb3, s->pair_cam, ksorted, iota, s->cam_order, np, st, 0, cbits));
-        void* tmp3 = nullptr;
-        CK(cudaMallocAsync(&tmp3, sb3, st));
-        CUBL(radix_sort_pairs(tmp3, sb3, s->pair_cam, ksorted, iota, s->cam_order, np, st, 0, cbits));
-        cudaFreeAsync(tmp3, st);
-        s->release(ksorted);
-        s->release(iota);
-      }
+      if (kept_pairs > 0)
+        KL(launch_cam_scatter(s->tile_off, s->n_tiles, cap, s->pair_cam, s->pair_tile, camtile, wordpre, tw,
+                              s->cam_off, s->cam_order, st));
+      s->release(wordpre);
       KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
     }
+    s->release(camtile);
     CK(cudaEventRecord(s->ev[12], st));
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
@@ -1315,7 +1314,6 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->st.n_cameras = n_cams;
     s->st.n_local_cameras = s->N_loc;
     s->st.cam_begin = s->cam_begin;
-    s->st.tile_pairs = (uint64_t)np;
     return LOBE_OK;
   }();
   if (rs != LOBE_OK) {

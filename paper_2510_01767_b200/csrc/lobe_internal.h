@@ -145,7 +145,13 @@ cudaError_t launch_tile_count(const uint32_t* koff, const uint8_t* nonempty, int
 cudaError_t exclusive_scan_u32(void* tmp, size_t& tmp_bytes, const uint32_t* in, uint32_t* out, int64_t n,
                                cudaStream_t st);
 cudaError_t launch_tile_fill(const uint32_t* koff, const uint32_t* klist, const uint8_t* nonempty, int64_t n_tiles,
-                             const uint32_t* offsets, uint32_t* pair_cam, uint32_t* pair_tile, cudaStream_t st);
+                             const uint32_t* offsets, uint32_t* pair_cam, uint32_t* pair_tile, uint32_t* camtile,
+                             int64_t tw, cudaStream_t st);
+cudaError_t launch_cam_order(int64_t n_cams, int64_t tw, const uint32_t* camtile, uint32_t* wordpre,
+                             uint32_t* counts, cudaStream_t st);
+cudaError_t launch_cam_scatter(const uint32_t* tile_off, int64_t n_tiles, int64_t cap, const uint32_t* pair_cam,
+                               const uint32_t* pair_tile, const uint32_t* camtile, const uint32_t* wordpre,
+                               int64_t tw, const uint32_t* cam_off, int32_t* cam_order, cudaStream_t st);
 
 // a5: per-Gaussian zone pair, per-word / per-tile uniform zone, per-zone counts.
 cudaError_t launch_zones(const ZoneTables* dz, int nzv, int nzp, int64_t G, int64_t G_pad, const float* gu,
