@@ -1036,12 +1036,12 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       for (int k = 0; k < 11; ++k) din[k] = src[k];
     }
     // ---- a1 precompute
-    float *ru, *rv, *kk;
+
     float4* rec;
     uint32_t *keys, *keys_s, *scratch;
     int32_t *vals, *perm;
     unsigned long long* err_idx;
-    CK(s->alloc(&ru, G)); CK(s->alloc(&rv, G)); CK(s->alloc(&kk, G));
+
     float* cov_raw = nullptr;  // anisotropic: Sigma per Gaussian, caller order
     if (s->aniso) CK(s->alloc(&cov_raw, (size_t)6 * G));
     CK(s->alloc(&rec, (size_t)2 * G));
@@ -1062,12 +1062,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     pin.rho = F.radius;
     pin.cov = cov_raw;
-    KL(launch_prep_raw(pin, ru, rv, kk, keys, vals, scratch, err_idx, scratch + 1, st));
+    KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
     // validation flags and the ground min / max reach the host asynchronously;
     // they are checked at the first synchronisation (after the culling pass)
     CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), cudaMemcpyDeviceToHost, st));
-    KL(launch_prep_norm(G, ru, rv, scratch + 1, din[0], din[1], din[2], kk, din[10], rec, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));  // top 24 of the 30-bit Morton keys
     void* tmp = nullptr;
@@ -1080,10 +1079,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
     CK(s->alloc(&s->iperm, (size_t)G));
     if (s->aniso) CK(s->alloc(&s->cv, (size_t)s->G_pad / 2 * 3));
-    KL(launch_pack(G, s->G_pad, perm, rec, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st));
+    KL(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st));
     s->release(cov_raw);
     cudaFreeAsync(tmp, st);
-    s->release(ru); s->release(rv); s->release(kk); s->release(rec);
+    s->release(rec);
     s->release(keys); s->release(keys_s); s->release(vals); s->release(perm);
     s->release(err_idx);
     if (dev_in) s->release(dev_in);
@@ -1420,12 +1419,10 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
     if (elig_dev) de = reinterpret_cast<uint32_t*>(eligible);
     else CK(s->alloc(&de, bytes / 4));
   }
-  uint64_t* mbits = nullptr;
-  uint8_t* cb8 = nullptr;
-  CK(s->alloc(&mbits, (size_t)s->words * 32));
-  CK(s->alloc(&cb8, (size_t)s->words * 32));
+  uint4* mrec = nullptr;
+  CK(s->alloc(&mrec, (size_t)s->words * 32));
   CK(cudaEventRecord(s->ev[14], s->stream));
-  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream));
+  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mrec, dc, de, s->stream));
   CK(cudaEventRecord(s->ev[15], s->stream));
   if (crop && !crop_dev) {
     TRY(copy_out(s, crop, dc, bytes));
@@ -1435,8 +1432,7 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
     TRY(copy_out(s, eligible, de, bytes));
     s->release(de);
   }
-  s->release(mbits);
-  s->release(cb8);
+  s->release(mrec);
   if ((crop && !crop_dev) || (eligible && !elig_dev)) {
     CK(cudaStreamSynchronize(s->stream));  // host outputs are complete on return
     s->st.t_crop_ms = ms_between(s->ev[14], s->ev[15]);
@@ -1568,14 +1564,11 @@ lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t bl
   CK(s->alloc(&dc, (size_t)g.B * W64));
   CK(s->alloc(&de, (size_t)g.B * W64));
   {
-    uint64_t* mbits = nullptr;
-    uint8_t* cb8 = nullptr;
-    CK(s->alloc(&mbits, (size_t)s->words * 32));
-    CK(s->alloc(&cb8, (size_t)s->words * 32));
-    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
+    uint4* mrec = nullptr;
+    CK(s->alloc(&mrec, (size_t)s->words * 32));
+    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mrec,
                    reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st));
-    s->release(mbits);
-    s->release(cb8);
+    s->release(mrec);
   }
   const uint64_t* cb = dc + (size_t)block * W64;
   const uint64_t* eb = de + (size_t)block * W64;

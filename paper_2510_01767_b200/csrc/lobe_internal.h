@@ -69,23 +69,21 @@ static_assert(sizeof(AnisoCam) == 96, "AnisoCam layout");
 // k = 3 max(s); anisotropic: k = trace(Sigma) and Sigma into in.cov). err[0] =
 // error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
 // Also writes the 3D Morton sort key of the contracted centre and identity values.
-cudaError_t launch_prep_raw(const PrepIn& in, float* ru, float* rv, float* kk, uint32_t* keys, int32_t* vals,
-                            uint32_t* err, unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
+cudaError_t launch_prep_raw(const PrepIn& in, float4* rec, uint32_t* keys, int32_t* vals, uint32_t* err,
+                            unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
 // Normalise the ground coordinates to [0,1].
 cudaError_t launch_cam_grid(int64_t N, const float* ru, const float* rv, const uint32_t* mm_ord, float* gu, float* gv,
                             cudaStream_t st);
-cudaError_t launch_prep_norm(int64_t G, const float* ru, const float* rv, const uint32_t* mm_ord, const float* x,
-                             const float* y, const float* z, const float* kk, const float* o, float4* rec,
-                             cudaStream_t st);
+
 // stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit)
 cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                              int32_t* vout, int64_t n, cudaStream_t st, int begin_bit = 0, int end_bit = 32);
 // Gather into the internal pair-interleaved layout, build the inverse permutation;
 // anisotropic: also Sigma, cv[3 (32 g + l) + {0,1,2}] = {S00A,S00B,S01A,S01B},
 // {S02A,S02B,S11A,S11B}, {S12A,S12B,S22A,S22B}.
-cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float4* rec, float* xy, float* zk,
-                        float* o2, float* gu, float* gv, int32_t* iperm, const float* cov_raw, float4* cv,
-                        cudaStream_t st);
+cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float4* rec, const uint32_t* mm_ord,
+                        float* xy, float* zk, float* o2, float* gu, float* gv, int32_t* iperm, const float* cov_raw,
+                        float4* cv, cudaStream_t st);
 
 // a3: visibility tests -> rows, tile flags, per-(chunk,camera) partials.
 struct VisArgs {
@@ -190,9 +188,9 @@ cudaError_t launch_masks_combine(const uint32_t* gathered, int W, int B, int64_t
                                  uint32_t* gvis, cudaStream_t st);
 // a9: caller-order crop / eligible masks.
 // mt: scratch, B x words u32 (word-major transpose of masks)
-// a9: per-Gaussian block bits (scratch mbits, cb8: words * 32 entries each), then the caller-order gather
+// a9: per-Gaussian block bits + cell block (scratch mrec: words * 32 records), then the caller-order gather
 cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint8_t* zp_cellblock,
-                        const uint32_t* masks, int64_t words, int B, uint64_t* mbits, uint8_t* cb8, uint32_t* crop32,
+                        const uint32_t* masks, int64_t words, int B, uint4* mrec, uint32_t* crop32,
                         uint32_t* elig32, cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
                                int64_t count, const uint32_t* keep, int64_t n_sub, uint32_t* out, cudaStream_t st);
