@@ -1419,10 +1419,12 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
     if (elig_dev) de = reinterpret_cast<uint32_t*>(eligible);
     else CK(s->alloc(&de, bytes / 4));
   }
-  uint4* mrec = nullptr;
-  CK(s->alloc(&mrec, (size_t)s->words * 32));
+  uint64_t* mbits = nullptr;
+  uint8_t* cb8 = nullptr;
+  CK(s->alloc(&mbits, (size_t)s->words * 32));
+  CK(s->alloc(&cb8, (size_t)s->words * 32));
   CK(cudaEventRecord(s->ev[14], s->stream));
-  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mrec, dc, de, s->stream));
+  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream));
   CK(cudaEventRecord(s->ev[15], s->stream));
   if (crop && !crop_dev) {
     TRY(copy_out(s, crop, dc, bytes));
@@ -1432,7 +1434,8 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
     TRY(copy_out(s, eligible, de, bytes));
     s->release(de);
   }
-  s->release(mrec);
+  s->release(mbits);
+  s->release(cb8);
   if ((crop && !crop_dev) || (eligible && !elig_dev)) {
     CK(cudaStreamSynchronize(s->stream));  // host outputs are complete on return
     s->st.t_crop_ms = ms_between(s->ev[14], s->ev[15]);
@@ -1564,11 +1567,14 @@ lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t bl
   CK(s->alloc(&dc, (size_t)g.B * W64));
   CK(s->alloc(&de, (size_t)g.B * W64));
   {
-    uint4* mrec = nullptr;
-    CK(s->alloc(&mrec, (size_t)s->words * 32));
-    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mrec,
+    uint64_t* mbits = nullptr;
+    uint8_t* cb8 = nullptr;
+    CK(s->alloc(&mbits, (size_t)s->words * 32));
+    CK(s->alloc(&cb8, (size_t)s->words * 32));
+    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
                    reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st));
-    s->release(mrec);
+    s->release(mbits);
+    s->release(cb8);
   }
   const uint64_t* cb = dc + (size_t)block * W64;
   const uint64_t* eb = de + (size_t)block * W64;

@@ -188,9 +188,9 @@ cudaError_t launch_masks_combine(const uint32_t* gathered, int W, int B, int64_t
                                  uint32_t* gvis, cudaStream_t st);
 // a9: caller-order crop / eligible masks.
 // mt: scratch, B x words u32 (word-major transpose of masks)
-// a9: per-Gaussian block bits + cell block (scratch mrec: words * 32 records), then the caller-order gather
+// a9: per-Gaussian block bits (scratch mbits, cb8: words * 32 entries each), then the caller-order gather
 cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint8_t* zp_cellblock,
-                        const uint32_t* masks, int64_t words, int B, uint4* mrec, uint32_t* crop32,
+                        const uint32_t* masks, int64_t words, int B, uint64_t* mbits, uint8_t* cb8, uint32_t* crop32,
                         uint32_t* elig32, cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
                                int64_t count, const uint32_t* keep, int64_t n_sub, uint32_t* out, cudaStream_t st);
