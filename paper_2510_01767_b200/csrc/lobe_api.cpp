@@ -39,6 +39,21 @@ namespace {
 
 thread_local std::string g_err;
 
+// stream-ordered allocation; LOBE_TRACE_ALLOC=1 prints slow calls (pool growth)
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t st) {
+  static const bool trace = std::getenv("LOBE_TRACE_ALLOC") != nullptr;
+  if (!trace) return cudaMallocAsync(p, bytes, st);
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaMallocAsync(p, bytes, st);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > 0.5) std::fprintf(stderr, "[lobe] cudaMallocAsync %.1f MB: %.2f ms\n", bytes / 1e6, ms);
+  return e;
+}
+template <class T>
+cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
+  return malloc_async(reinterpret_cast<void**>(p), bytes, st);
+}
+
 lobe_status fail(lobe_status st, const std::string& msg) {
   g_err = msg;
   return st;
@@ -195,7 +210,7 @@ struct lobe_scene {
   cudaError_t alloc(T** p, size_t count) {
     *p = nullptr;
     if (count == 0) count = 1;
-    return cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), stream);
+    return malloc_async(reinterpret_cast<void**>(p), count * sizeof(T), stream);
   }
   template <class T>
   void release(T*& p) {
@@ -609,7 +624,7 @@ lobe_status scan_counts(lobe_scene* s, const uint32_t* cnt, uint32_t* off, int64
   size_t tb = 0;
   CK(exclusive_scan_u32(nullptr, tb, cnt, off, n + 1, st));
   void* tmp = nullptr;
-  CK(cudaMallocAsync(&tmp, tb, st));
+  CK(malloc_async(&tmp, tb, st));
   CUBL(exclusive_scan_u32(tmp, tb, cnt, off, n + 1, st));
   cudaFreeAsync(tmp, st);
   uint32_t t = 0;
@@ -645,20 +660,26 @@ lobe_status scratch(lobe_scene* s, RenderJob& J, int k, T** out, size_t count) {
   const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
   RenderJob::Buf& b = J.b[k];
   if (b.cap < bytes) {
-    if (b.p) cudaFreeAsync(b.p, s->stream);
+    // 1.5x headroom: later batches rarely need a new block. Plain cudaMalloc:
+    // these multi-GB blocks would otherwise grow the stream-ordered pool (slow)
+    const size_t cap = std::max(bytes, b.cap * 3 / 2);
+    if (b.p) {
+      CK(cudaStreamSynchronize(s->stream));
+      cudaFree(b.p);
+    }
     b.p = nullptr;
     b.cap = 0;
-    const size_t cap = std::max(bytes, b.cap * 3 / 2);
-    CK(cudaMallocAsync(&b.p, cap, s->stream));
+    CK(cudaMalloc(&b.p, cap));
     b.cap = cap;
   }
   *out = static_cast<T*>(b.p);
   return LOBE_OK;
 }
 void free_scratch(lobe_scene* s, RenderJob& J) {
+  cudaStreamSynchronize(s->stream);
   for (auto& b : J.b)
     if (b.p) {
-      cudaFreeAsync(b.p, s->stream);
+      cudaFree(b.p);
       b.p = nullptr;
       b.cap = 0;
     }
@@ -688,7 +709,7 @@ lobe_status grow_cloud(lobe_scene* s, RenderJob& J, int64_t need) {
 }
 
 // Render cameras [c0, c1) of the local shard and append their clouds.
-lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, const std::vector<uint32_t>& hoff,
+lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<uint32_t>& hoff,
                          const std::vector<lobe_camera>& hcams, int64_t c0, int64_t c1, RenderJob& J) {
   cudaStream_t st = s->stream;
   const int ncam = (int)(c1 - c0);
@@ -748,7 +769,7 @@ lobe_status render_batch(lobe_scene* s, const SubArgs& g, const int32_t* perm, c
   TRY(scratch(s, J, 8, &rec, N1 * 10));
   TRY(scratch(s, J, 9, &dseg, (size_t)ncam + 1));
   CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
-  KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, perm, g, drc,
+  KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, prec, drc,
                       keys, vals, rec, rcam, st));
   // 2. front to back per camera: (zc, caller index) -- one radix sort on
   //    (camera, zc bits), then runs of equal depth ordered by caller index
@@ -1070,7 +1091,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));  // top 24 of the 30-bit Morton keys
     void* tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, tmpb, st));
+    CK(malloc_async(&tmp, tmpb, st));
     CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));
     CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
@@ -1149,7 +1170,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       size_t sbk = 0;
       CK(exclusive_scan_u32(nullptr, sbk, kc, s->koff, s->n_tiles + 1, st));
       void* tk = nullptr;
-      CK(cudaMallocAsync(&tk, sbk, st));
+      CK(malloc_async(&tk, sbk, st));
       CUBL(exclusive_scan_u32(tk, sbk, kc, s->koff, s->n_tiles + 1, st));
       cudaFreeAsync(tk, st);
       s->release(kc);
@@ -1164,7 +1185,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       size_t sbu = 0;
       CK(exclusive_scan_u32(nullptr, sbu, uc, uoff, s->n_tiles + 1, st));
       void* tu = nullptr;
-      CK(cudaMallocAsync(&tu, sbu, st));
+      CK(malloc_async(&tu, sbu, st));
       CUBL(exclusive_scan_u32(tu, sbu, uc, uoff, s->n_tiles + 1, st));
       cudaFreeAsync(tu, st);
     }
@@ -1237,7 +1258,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     if (s->N_loc > 0 && kept_pairs > 0) KL(launch_tile_count(s->koff, s->nonempty, s->n_tiles, cnt, st));
     size_t sb = 0;
     CK(exclusive_scan_u32(nullptr, sb, cnt, s->tile_off, s->n_tiles + 1, st));
-    CK(cudaMallocAsync(&tmp, sb, st));
+    CK(malloc_async(&tmp, sb, st));
     CUBL(exclusive_scan_u32(tmp, sb, cnt, s->tile_off, s->n_tiles + 1, st));
     cudaFreeAsync(tmp, st);
     s->release(cnt);
@@ -1273,7 +1294,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       size_t sb2 = 0;
       CK(exclusive_scan_u32(nullptr, sb2, ccount, s->cam_off, NL + 1, st));
       void* tmp2 = nullptr;
-      CK(cudaMallocAsync(&tmp2, sb2, st));
+      CK(malloc_async(&tmp2, sb2, st));
       CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
       cudaFreeAsync(tmp2, st);
       s->release(ccount);
@@ -1727,6 +1748,10 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
   int32_t* perm = nullptr;
   CK(s->alloc(&perm, (size_t)s->G_pad));
   KL(launch_perm_from_iperm(s->G, s->iperm, perm, st));
+  float4* prec = nullptr;
+  CK(s->alloc(&prec, (size_t)3 * std::max<int64_t>(s->G, 1)));
+  KL(launch_render_prep(s->G, perm, g, prec, st));
+  s->release(perm);
   const int64_t NL = s->N_loc;
   std::vector<uint32_t> hoff(NL + 1), hK(std::max<int64_t>(NL, 1));
   CK(cudaMemcpyAsync(hoff.data(), s->cam_off, sizeof(uint32_t) * (NL + 1), cudaMemcpyDeviceToHost, st));
@@ -1742,7 +1767,7 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
     uint64_t recs = 0;
     while (e < ce && (e == c || recs + hK[e] <= kBudget) && e - c < 2048) recs += hK[e++];
     const auto t0 = std::chrono::steady_clock::now();
-    TRY(render_batch(s, g, perm, hoff, hcams, c, e, J));
+    TRY(render_batch(s, prec, hoff, hcams, c, e, J));
     if (trace) {
       CK(cudaStreamSynchronize(st));
       const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1751,7 +1776,7 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
     }
     c = e;
   }
-  s->release(perm);
+  s->release(prec);
   free_scratch(s, J);
   if (cloud_counts) {
     // cloud size per local camera (integer atomics: order-free)
