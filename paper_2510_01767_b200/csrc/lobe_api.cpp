@@ -74,6 +74,12 @@ lobe_status fail(lobe_status st, const std::string& msg) {
     CK(call);                         \
     s->st.kernel_launches += 1;       \
   } while (0)
+// a launcher that starts n kernels (launch_cull, launch_crop: 2)
+#define KLN(call, n)                  \
+  do {                                \
+    CK(call);                         \
+    s->st.kernel_launches += (n);     \
+  } while (0)
 #define CUBL(call)                    \
   do {                                \
     CK(call);                         \
@@ -1156,7 +1162,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
-    if (s->N_loc > 0) KL(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, st));
+    if (s->N_loc > 0) KLN(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, st), 2);
     CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
     unsigned long long kept_pairs = 0;
@@ -1445,7 +1451,7 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   CK(s->alloc(&mbits, (size_t)s->words * 32));
   CK(s->alloc(&cb8, (size_t)s->words * 32));
   CK(cudaEventRecord(s->ev[14], s->stream));
-  KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream));
+  KLN(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream), 2);
   CK(cudaEventRecord(s->ev[15], s->stream));
   if (crop && !crop_dev) {
     TRY(copy_out(s, crop, dc, bytes));
@@ -1592,8 +1598,8 @@ lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t bl
     uint8_t* cb8 = nullptr;
     CK(s->alloc(&mbits, (size_t)s->words * 32));
     CK(s->alloc(&cb8, (size_t)s->words * 32));
-    KL(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
-                   reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st));
+    KLN(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
+                   reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st), 2);
     s->release(mbits);
     s->release(cb8);
   }
