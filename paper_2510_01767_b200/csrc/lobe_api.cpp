@@ -183,6 +183,8 @@ struct lobe_scene {
     unsigned long long vc[8];               // k_vis_tiles counters of the last pass
     uint32_t prep_hs[8];                    // k_prep_raw: error flags, ordered ground min / max
     uint32_t n_pairs;                       // non-empty (tile, camera) pairs of the last load
+    uint32_t n_units;                       // visibility work units of the last load
+    unsigned long long kept_pairs;          // (tile, camera) pairs kept by the culling pass
     unsigned long long prep_bad;            // k_prep_raw: first invalid Gaussian
   };
   static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
@@ -1165,8 +1167,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     if (s->N_loc > 0) KLN(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, st), 2);
     CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
-    unsigned long long kept_pairs = 0;
-    CK(cudaMemcpyAsync(&kept_pairs, s->kept, sizeof(kept_pairs), cudaMemcpyDeviceToHost, st));
+    // list sizes go to pinned memory: the copies do not block the host, which
+    // keeps enqueueing until the one synchronisation below
+    CK(cudaMemcpyAsync(&s->pin->kept_pairs, s->kept, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(s->alloc(&s->koff, (size_t)s->n_tiles + 1));
     {
       uint32_t* kc;
@@ -1195,9 +1198,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       CUBL(exclusive_scan_u32(tu, sbu, uc, uoff, s->n_tiles + 1, st));
       cudaFreeAsync(tu, st);
     }
-    uint32_t nu = 0;
-    CK(cudaMemcpyAsync(&nu, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&s->pin->n_units, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    const unsigned long long kept_pairs = s->pin->kept_pairs;
+    const uint32_t nu = s->pin->n_units;
     s->n_units = nu;
     {  // k_prep_raw's verdict (its copies completed with this synchronisation)
       const uint32_t* hs = s->pin->prep_hs;
