@@ -102,6 +102,17 @@ def test_ragged_multi_tile():
                      oracle.default_grid(1, 7), oracle.default_grid(2, 2, tau=1.0)])
 
 
+@pytest.mark.parametrize("groups", ["1", "2"])
+def test_block_masks_group_overflow(groups, monkeypatch):
+    """k_block_masks groups a tile's cameras by assignment set in a 64-slot hash
+    table; with the table cut to 1 or 2 slots (LOBE_MASK_GROUPS, read at every
+    launch) most cameras take the direct path. Loads and crop masks must not
+    change."""
+    monkeypatch.setenv("LOBE_MASK_GROUPS", groups)
+    sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x5151))
+    full_parity(sc, [_rand_grid(8, 8, 4, tau=0.05), oracle.default_grid(4, 4)])
+
+
 def test_mid_size():
     sc = make_scene(make_config("matrixcity", G=150_000, N=120, seed=0x77))
     full_parity(sc, [oracle.default_grid(6, 6), _rand_grid(5, 4, 9)])
