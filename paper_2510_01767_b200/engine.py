@@ -8,7 +8,9 @@ between ranks with torch.distributed (NCCL over NVLink on GPUs, gloo in the
 CPU tests) and calls back into the library for the OR-combine / popcount
 kernel:
 
-  per evaluation   all_gather(partial masks, B x words u32)  ->  lobe_masks_combine (OR + popcount)
+  per evaluation   all_to_all(partial masks of each rank's own blocks)
+                   ->  lobe_masks_combine (OR of the W partials + popcount, own blocks only)
+                   all_gather(combined masks of the own blocks), all_gather(G_vis of the own blocks)
                    all_reduce(SUM, |C^(b)| and I_b)          ->  lobe_block_records
   per-camera data  all_gather (padded to the largest shard)
 
@@ -85,12 +87,31 @@ class Engine:
         if self._comb_key == key and self._loads is not None:
             return self._loads  # this grid was already exchanged (e.g. by crop_masks first)
         B = m * n
+        W, r = self.world, self.rank
         words = self.local.mask_words()
         part = torch.zeros(B * words, dtype=torch.int32, device=self.device)
         nc, inc = self.local.block_partial(m, n, part, **grid_kw)
-        gathered = self._all_gather_flat(part)
-        comb = torch.empty_like(part)
-        gv = self.local.masks_combine(B, gathered, self.world, comb)
+        # OR reduce-scatter by blocks: rank j owns blocks [floor(jB/W), floor((j+1)B/W));
+        # each rank sends every other rank the partial masks of that rank's
+        # blocks (one all_to_all), then ORs the W partials of its own blocks
+        # and popcounts them with lobe_masks_combine
+        nb = [shard(B, j, W)[1] - shard(B, j, W)[0] for j in range(W)]
+        recv = torch.empty(W * nb[r] * words, dtype=torch.int32, device=self.device)
+        dist.all_to_all_single(recv, part, output_split_sizes=[nb[r] * words] * W,
+                               input_split_sizes=[k * words for k in nb], group=self.group)
+        own = torch.zeros(nb[r] * words, dtype=torch.int32, device=self.device)
+        gv_own = self.local.masks_combine(nb[r], recv, W, own) if nb[r] > 0 else np.zeros(0, np.uint32)
+        # every rank needs the combined masks of all blocks for the crop: one
+        # all_gather of the owned slices, padded to the largest share
+        P = max(nb)
+        buf = torch.zeros(P * words, dtype=torch.int32, device=self.device)
+        buf[:nb[r] * words] = own
+        gat = self._all_gather_flat(buf).view(W, P * words)
+        comb = torch.cat([gat[j, :nb[j] * words] for j in range(W)])
+        gvb = torch.zeros(P, dtype=torch.int64, device=self.device)
+        gvb[:nb[r]] = torch.from_numpy(np.asarray(gv_own, np.int64)).to(self.device)
+        gva = self._all_gather_flat(gvb).view(W, P).cpu().numpy()
+        gv = np.concatenate([gva[j, :nb[j]] for j in range(W)]).astype(np.uint32)
         counts = torch.from_numpy(np.concatenate([nc.astype(np.int64), inc.astype(np.int64)])).to(self.device)
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
         counts = counts.cpu().numpy()

@@ -1,9 +1,11 @@
 """The multi-rank exchange (paper_2510_01767_b200/engine.py) on
-CPU with the gloo backend, world sizes 2 and 3.
+CPU with the gloo backend, world sizes 2, 3 and 5 (5 ranks share the 12
+blocks unevenly: the block-sharded OR reduce-scatter pads the gathers).
 
 Each rank's local backend here is the oracle restricted to the rank's camera
 shard (test infrastructure); the choreography under test -- shard ranges,
-all_gather layout of the partial masks, OR-combine, count all_reduce,
+all_to_all of the partial masks by owned blocks, OR-combine, all_gather of
+the combined masks and counts, count all_reduce,
 per-camera all_gather with padding -- is the engine's own code, the same that
 runs over NCCL on GPUs. Results must equal the world = 1 oracle (I12).
 """
@@ -111,7 +113,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 5])
 def test_gloo_engine_matches_world1(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
