@@ -399,6 +399,18 @@ def main():
             "logical_frac_of_dense_roofline": (FLOP_PER_TEST * G * n_local / (peak * 1e12) * 1e3) / t_vis,
             "target_logical_tests_per_s": 0.6 * peak * 1e12 / FLOP_PER_TEST,
             "frac_at_measured_clock": (achieved / (peak * (clocks["sm_mhz"] or sm_max_mhz) / sm_max_mhz))}
+    # the depth statistic (a4), the other large kernel of the step: 9 flop per
+    # visible (Gaussian, camera) incidence (w: 3 FMA, o*w: 1 FMA, o: 1 add), the
+    # statistic's own work; the kernel evaluates w for every Gaussian of each
+    # non-empty 256-Gaussian slice and adds min / max and the reductions
+    vis_inc = int(np.asarray(Aout["K"], np.int64).sum())
+    from paper_2510_01767_b200.engine import shard
+    c0, c1 = shard(N, rank, world)
+    depth_flop = 9.0 * float(np.asarray(Aout["K"][c0:c1], np.int64).sum())  # this rank's cameras
+    depth_roof = {"bound": "alu", "kernel": "k_depth_pairs + camera order + k_depth_reduce (a4)",
+                  "achieved": depth_flop / (t_depth * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                  "frac": depth_flop / (t_depth * 1e-3) / 1e12 / peak, "kernel_ms": t_depth,
+                  "flop_basis": "9 flop per visible (Gaussian, camera) incidence of this rank's cameras"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(sc, pred=pred)
@@ -411,7 +423,7 @@ def main():
                        "parallelism": f"camera-sharded x{world}", "l2": "inputs larger than L2 (no flush)",
                        "step": "a1-a9 (+a11 exchange): load+precompute+sort, visibility, assignment, block loads "
                                "at uniform cuts, crop masks", "seed": hex(sc.cfg.seed)},
-            "roofline": roof, "cpu_baseline": cpu,
+            "roofline": roof, "depth_roofline": depth_roof, "cpu_baseline": cpu,
             "e2e": {"value": G * N / (ms_e2e * 1e-3), "unit": "tests/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
             "gpu_launches": int(timed_kernels),
@@ -420,7 +432,7 @@ def main():
                                  f"(radix sort, scan): {timed_cub / args.steps:.0f} per step",
             "clocks": clocks, "bo": bo,
             "objective_uniform": int(Lrec["objective"]),
-            "visible_incidences": int(np.asarray(Aout["K"], np.int64).sum()),
+            "visible_incidences": vis_inc,
             "tile_pairs": int(stats_acc["pairs"]),
             "hashes": array_hashes(sc) if cfg_name != "matrixcity" else None}
     print(json.dumps(line), flush=True)
