@@ -378,7 +378,7 @@ def main():
         except Exception:
             pass
     clocks = clk.summary()
-    roof = {"bound": "alu", "kernel": "k_cull + k_vis_tiles%s (a3)" % ("_aniso" if pred else ""), "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": "alu", "kernel": ("k_cull + k_vis_tiles_aniso (a3)" if pred else "k_cull + k_slice_codes + k_vis_tiles (a3)"), "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max_mhz:.0f} MHz "
                           "(sm_max_mhz of MEASURED_PEAKS.json); %d flop/test" % FLOP_PER_TEST,

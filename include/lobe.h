@@ -175,7 +175,7 @@ typedef struct {
                                rejected tiles/slices (no Gaussian visible) or accepted slices (every
                                non-gated Gaussian visible) -- identical results, see k_vis_tiles */
   double t_cull_ms;         /* tile-culling kernel of the last visibility pass (included in t_vis_ms,
-                               which is culling + test kernels) */
+                               which is culling + slice classification + test kernels) */
   double t_depth_ms;        /* depth statistic over the non-empty (tile, camera) pairs (a4) */
   uint64_t kernel_launches; /* cumulative launches of this library's own kernels */
   uint64_t cub_launches;    /* cumulative CUB primitive calls (radix sort, scan) */

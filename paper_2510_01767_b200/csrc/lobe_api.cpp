@@ -128,6 +128,7 @@ struct lobe_scene {
   int32_t* cam_order = nullptr;
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
   float4 *slice_lo = nullptr, *slice_hi = nullptr;
+  uint32_t* codes = nullptr;  // per kept pair: slice classes (k_slice_codes)
   bool aniso = false;            // anisotropic predicate (ledger L24)
   float4* cv = nullptr;          // pair-interleaved Sigma (anisotropic)
   AnisoCam* acams = nullptr;     // per local camera (anisotropic)
@@ -212,7 +213,7 @@ struct lobe_scene {
   const unsigned long long* h_incid() { wait_counts(); return pin->incid; }
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[16] = {};  // load pass: 0, 1, 8-12; evaluation: 2-4, 13; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
+  cudaEvent_t ev[18] = {};  // load pass: 0, 1, 8-12, 16, 17; evaluation: 2-4, 13; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -858,7 +859,9 @@ void finalize_load_stats(lobe_scene* s) {
   s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
   // visibility pass = culling kernel + test kernel (list building excluded)
   s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
-  s->st.t_vis_ms = s->st.t_cull_ms + ms_between(s->ev[9], s->ev[10]);
+  // slice classification (k_slice_codes) is part of the test decision
+  const float t_codes = (!s->aniso && s->kept_pairs_last > 0) ? ms_between(s->ev[16], s->ev[17]) : 0.f;
+  s->st.t_vis_ms = s->st.t_cull_ms + t_codes + ms_between(s->ev[9], s->ev[10]);
   s->st.t_depth_ms = ms_between(s->ev[11], s->ev[12]);
   s->n_pairs = s->pin->n_pairs;
   s->st.tile_pairs = (uint64_t)s->n_pairs;
@@ -974,7 +977,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -1175,7 +1178,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       uint32_t* kc;
       CK(s->alloc(&kc, (size_t)s->n_tiles + 1));
       CK(cudaMemsetAsync(kc, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
-      if (s->N_loc > 0) KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, kc, nullptr, nullptr, 0, st));
+      if (s->N_loc > 0) KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, kc, nullptr, nullptr, nullptr, 0, st));
       size_t sbk = 0;
       CK(exclusive_scan_u32(nullptr, sbk, kc, s->koff, s->n_tiles + 1, st));
       void* tk = nullptr;
@@ -1223,11 +1226,20 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     CK(s->alloc(&s->klist, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(s->alloc(&s->nonempty, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
+    CK(s->alloc(&s->codes, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
     CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
     CK(s->alloc(&s->queue, 1));
     if (s->N_loc > 0 && kept_pairs > 0) {
-      KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, 1, st));
+      uint32_t* tlist = nullptr;  // tile of each kept pair (k_slice_codes only)
+      if (!s->aniso) CK(s->alloc(&tlist, (size_t)kept_pairs));
+      KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, tlist, 1, st));
+      if (!s->aniso) {
+        CK(cudaEventRecord(s->ev[16], st));
+        KL(launch_slice_codes((int64_t)kept_pairs, s->klist, tlist, s->cams, s->slice_lo, s->slice_hi, s->codes, st));
+        CK(cudaEventRecord(s->ev[17], st));
+        s->release(tlist);
+      }
       KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile, nu, 1, st));
     }
     s->release(uc);
@@ -1254,6 +1266,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.aniso = s->aniso;
       va.cv = s->cv;
       va.acams = s->acams;
+      va.codes = s->codes;
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
@@ -1562,6 +1575,7 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.aniso = s->aniso;
   va.cv = s->cv;
   va.acams = s->acams;
+  va.codes = s->codes;
   if (s->aniso && variant != 0) return fail(LOBE_E_INVALID_CONFIG, "camera-inner variants are isotropic only");
   int g = 0;
   auto run = [&]() -> cudaError_t {

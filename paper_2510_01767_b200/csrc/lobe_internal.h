@@ -105,6 +105,7 @@ struct VisArgs {
   int aniso;                     // 1: anisotropic predicate (ledger L24)
   const float4* cv;              // anisotropic: pair-interleaved Sigma
   const AnisoCam* acams;         // anisotropic: per local camera
+  const uint32_t* codes;         // k_vis_tiles (isotropic): per kept pair, the 4 slices' box_class codes (8 bits each)
 };
 
 // Tile culling: per camera the five linear forms of the
@@ -118,8 +119,13 @@ cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float
                         const CamSetup* cams, const AnisoCam* acams, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
                         cudaStream_t st);
 // kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
+// per kept (tile, camera) pair (klist order): byte q = box_class of slice q
+// (0 reject, 2 accept, 1 | need << 2 undecided), so the test kernel loads
+// camera parameters only for undecided slices
+cudaError_t launch_slice_codes(int64_t n_kept, const uint32_t* klist, const uint32_t* tlist, const CamSetup* cams,
+                               const float4* slo, const float4* shi, uint32_t* codes, cudaStream_t st);
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
-                              const uint32_t* offs, uint32_t* list, int phase, cudaStream_t st);
+                              const uint32_t* offs, uint32_t* list, uint32_t* tlist, int phase, cudaStream_t st);
 // tile-major visibility over the kept lists: work units = (tile, <= kVisUnit cameras)
 constexpr int kVisUnit = 64;
 cudaError_t launch_units(const uint32_t* koff, int64_t n_tiles, int cmax, uint32_t* uc, const uint32_t* uoff,
