@@ -158,6 +158,7 @@ def run_reference(args, cfg_name):
         return 0
     import oracle
     from synth import make_scene
+    pred = 1 if args.predicate == "aniso" else 0
     sc = make_scene(cfg_name)
     threads = oracle.nthreads()
     m, n = sc.cfg.m, sc.cfg.n
@@ -174,7 +175,10 @@ def run_reference(args, cfg_name):
     def step():
         sel = np.sort(rng.choice(sc.N, per_step, replace=False))
         pre["cam_gu_sel"], pre["cam_gv_sel"] = pre["cam_gu"][sel], pre["cam_gv"][sel]
-        vis = oracle.visibility(sc, pre, cams=sel, threads=threads)
+        if pred:
+            vis = oracle.visibility_aniso(sc, pre, cams=sel, threads=threads)
+        else:
+            vis = oracle.visibility(sc, pre, cams=sel, threads=threads)
         oracle.assign(sc, pre, vis, oracle.default_grid(m, n), threads=threads)
 
     for _ in range(args.warmup):
@@ -190,10 +194,12 @@ def run_reference(args, cfg_name):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg_name}-shaped", "G": sc.G, "N": sc.N, "grid": f"{m}x{n}"},
+            "config": {"workload": f"{cfg_name}-shaped", "G": sc.G, "N": sc.N, "grid": f"{m}x{n}",
+                       "predicate": "anisotropic (EWA, ledger L24)" if pred else "isotropic (SPEC.md:299)"},
             "cpu_baseline": {"value": value, "unit": "tests/s", "cores": threads, "kind": "oracle",
                              "sample": f"per step {per_step} random cameras x all {sc.G} Gaussians: visibility "
-                                       f"(O6/O7) + assignment (O8) + their share of the per-Gaussian prep"},
+                                       f"({'O6a' if pred else 'O6'}/O7) + assignment (O8) + their share of the "
+                                       f"per-Gaussian prep"},
             "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
