@@ -129,6 +129,7 @@ struct lobe_scene {
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
   float4 *slice_lo = nullptr, *slice_hi = nullptr;
   uint32_t* codes = nullptr;  // per kept pair: slice classes (k_slice_codes)
+  bool aniso_fast = true;     // anisotropic test may use the branch-free rcp / sqrt (all depth ranges in range)
   bool aniso = false;            // anisotropic predicate (ledger L24)
   float4* cv = nullptr;          // pair-interleaved Sigma (anisotropic)
   AnisoCam* acams = nullptr;     // per local camera (anisotropic)
@@ -1127,7 +1128,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     for (int64_t c = 0; c < s->N_loc; ++c) {  // host work overlapping the device's a1 pass
       const lobe_camera& k = cams[s->cam_begin + c];
       hset[c] = camera_setup(k);
-      if (s->aniso) haset[c] = aniso_setup(k);
+      if (s->aniso) {
+        haset[c] = aniso_setup(k);
+        // branch-free reciprocal / square root need depths in [2^-126, 2^126]
+        if (!(haset[c].zn >= 0x1p-126f && haset[c].zf <= 0x1p126f)) s->aniso_fast = false;
+      }
       double oc[3];
       cam_centre(k, oc);
       ground_uv_host((float)oc[0], (float)oc[1], (float)oc[2], F, &cam_ru[c], &cam_rv[c]);
@@ -1267,6 +1272,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.cv = s->cv;
       va.acams = s->acams;
       va.codes = s->codes;
+      va.aniso_fast = s->aniso_fast ? 1 : 0;
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
     }
@@ -1576,6 +1582,7 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   va.cv = s->cv;
   va.acams = s->acams;
   va.codes = s->codes;
+  va.aniso_fast = s->aniso_fast ? 1 : 0;
   if (s->aniso && variant != 0) return fail(LOBE_E_INVALID_CONFIG, "camera-inner variants are isotropic only");
   int g = 0;
   auto run = [&]() -> cudaError_t {

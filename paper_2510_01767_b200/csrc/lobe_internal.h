@@ -106,6 +106,7 @@ struct VisArgs {
   const float4* cv;              // anisotropic: pair-interleaved Sigma
   const AnisoCam* acams;         // anisotropic: per local camera
   const uint32_t* codes;         // k_vis_tiles (isotropic): per kept pair, the 4 slices' box_class codes (8 bits each)
+  int aniso_fast;                // anisotropic: every camera's depth range within [2^-126, 2^126] (branch-free rcp/sqrt)
 };
 
 // Tile culling: per camera the five linear forms of the
