@@ -205,7 +205,9 @@ const char* lobe_last_error(void);
  * V_c inside the enlarged regions / delta = 0 cells;
  * member: bit b set iff K_c > 0 and n_cb >= tau K_c;
  * home: lowest b maximising n0_cb, camera-centre cell if K_c = 0 (ledger L7/L8).
- * Any output pointer may be NULL. */
+ * Any output pointer may be NULL; host or device pointers. The outputs are
+ * complete on return. Copies into pageable host memory wait only for the end of
+ * the evaluation, not for later work on the scene's stream (e.g. a crop). */
 lobe_status lobe_assign_cameras(lobe_scene* scene, const lobe_grid* grid, uint32_t* K, double* depth_mean,
                                 float* z_min, float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member,
                                 int32_t* home);

@@ -130,6 +130,7 @@ struct lobe_scene {
   float4 *slice_lo = nullptr, *slice_hi = nullptr;
   uint32_t* codes = nullptr;  // per kept pair: slice classes (k_slice_codes)
   bool aniso_fast = true;     // anisotropic test may use the branch-free rcp / sqrt (all depth ranges in range)
+  cudaStream_t side = nullptr;  // per-camera host copies (run_staged), created on first use
   bool aniso = false;            // anisotropic predicate (ledger L24)
   float4* cv = nullptr;          // pair-interleaved Sigma (anisotropic)
   AnisoCam* acams = nullptr;     // per local camera (anisotropic)
@@ -917,6 +918,28 @@ void recycle_pinned_out(uint8_t* p, size_t cap) {
   g_pin_out_free.emplace_back(p, cap);
 }
 
+// Side streams for the per-camera copies, recycled across scenes (one per
+// live scene; creating a stream costs ~0.4 ms).
+std::vector<std::pair<int, cudaStream_t>> g_side_free;
+cudaStream_t acquire_side_stream(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_side_free.size(); ++i)
+      if (g_side_free[i].first == device) {
+        cudaStream_t st = g_side_free[i].second;
+        g_side_free.erase(g_side_free.begin() + i);
+        return st;
+      }
+  }
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return st;
+}
+void recycle_side_stream(int device, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_side_free.emplace_back(device, st);
+}
+
 // Per-camera outputs: asynchronous copies into pinned staging when the
 // destination is ordinary pageable host memory, one synchronisation, then host
 // copies into the caller's buffers (out_plan collects them).
@@ -937,8 +960,18 @@ lobe_status stage_out(lobe_scene* s, std::vector<StagedCopy>& plan, size_t& used
 }
 lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used,
                        const std::vector<const void*>& srcs) {
+  if (plan.empty()) {
+    CK(cudaStreamSynchronize(s->stream));
+    return LOBE_OK;
+  }
+  // The copies run on a side stream that waits only for the end of the last
+  // evaluation (ev[4]): kernels enqueued after it on the scene's stream (e.g.
+  // a crop) keep running while the host copies out.
+  if (!s->side) s->side = acquire_side_stream(s->device);
+  if (!s->side) return fail(LOBE_E_CUDA, "side stream creation failed");
   if (used > s->pin_out_cap) {
-    CK(cudaStreamSynchronize(s->stream));  // the old block may still be a copy target
+    CK(cudaStreamSynchronize(s->side));    // the old block may still be a copy target
+    CK(cudaStreamSynchronize(s->stream));
     recycle_pinned_out(s->pin_out, s->pin_out_cap);
     s->pin_out = acquire_pinned_out(used, &s->pin_out_cap);
     if (!s->pin_out) {
@@ -946,10 +979,12 @@ lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used
       return fail(LOBE_E_CUDA, "pinned staging allocation failed");
     }
   }
+  CK(cudaStreamWaitEvent(s->side, s->ev[4], 0));
   for (size_t i = 0; i < plan.size(); ++i)
-    CK(cudaMemcpyAsync(s->pin_out + plan[i].off, srcs[i], plan[i].bytes, cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpyAsync(s->pin_out + plan[i].off, srcs[i], plan[i].bytes, cudaMemcpyDeviceToHost, s->side));
+  CK(cudaStreamSynchronize(s->side));
   for (const auto& c : plan) std::memcpy(c.dst, s->pin_out + c.off, c.bytes);
+  CK(cudaEventSynchronize(s->ev[4]));  // device destinations (scene stream) are ordered after it anyway
   return LOBE_OK;
 }
 
@@ -986,6 +1021,10 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->ncb); s->release(s->n0cb); s->release(s->member); s->release(s->sel); s->release(s->home);
   s->release(s->counts); s->incid = nullptr; s->release(s->masks);
   cudaStreamSynchronize(s->stream);
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    recycle_side_stream(s->device, s->side);  // stream creation costs ~0.4 ms: reuse across scenes
+  }
   for (auto& e : s->ev)
     if (e) cudaEventDestroy(e);
   recycle_pinned(s->pin);
@@ -1388,10 +1427,12 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
   std::vector<StagedCopy> plan;
   std::vector<const void*> srcs;
   size_t used = 0;
+  bool direct = false;  // a copy went straight to a device / pinned destination on the scene's stream
   auto add = [&](void* dst, const void* src, size_t bytes) -> lobe_status {
     const size_t before = plan.size();
     TRY(stage_out(s, plan, used, dst, src, bytes));
     if (plan.size() != before) srcs.push_back(src);
+    else if (dst && bytes) direct = true;
     return LOBE_OK;
   };
   TRY(add(K, s->K, NL * 4));
@@ -1404,6 +1445,7 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
   TRY(add(member, s->member, NL * 8));
   TRY(add(home, s->home, NL * 4));
   TRY(run_staged(s, plan, used, srcs));
+  if (direct) CK(cudaStreamSynchronize(s->stream));  // outputs are complete on return
   return LOBE_OK;
 }
 
