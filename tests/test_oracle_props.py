@@ -237,3 +237,31 @@ def test_modes_home_and_union(small_scene, small_run):
     assert int(lh["n_cams"].sum()) == sc.N                      # every camera has exactly one home (I3)
     assert (lu["g_vis"] >= np.maximum(lh["g_vis"], out["loads"]["g_vis"])).all()
     assert (lu["n_cams"] >= lh["n_cams"]).all()
+
+
+# ------------------------------------------------------------------ D_c, z_min, z_max
+@pytest.mark.parametrize("which", ["tiny", "small"])
+def test_depth_statistic_float64_route(which, tiny_scene, tiny_run, small_scene, small_run):
+    """Ledger L4: D_c is the opacity-weighted mean camera depth over V_c and
+    z_min / z_max its extremes. Recomputed by another route -- the camera-frame
+    depth (R x + t)_z of each visible Gaussian in float64 from the caller's
+    extrinsics (not the oracle's fp32 setup rows), weighted by the caller's
+    opacities -- it must match the oracle within the fp32 rounding of w (1e-5).
+    A wrong row, sign, translation or weight fails this."""
+    sc, out = (tiny_scene, tiny_run) if which == "tiny" else (small_scene, small_run)
+    vis = _unpack_rows(out["vis"]["rows"], sc.G)
+    P = np.stack([sc.x, sc.y, sc.z], 1).astype(np.float64)
+    o = sc.opacity.astype(np.float64)
+    checked = 0
+    for c in range(sc.N):
+        idx = np.flatnonzero(vis[c])
+        if len(idx) == 0:
+            assert out["vis"]["D"][c] == 0.0
+            continue
+        depth = P[idx] @ sc.R[c].astype(np.float64)[2] + float(sc.t[c][2])
+        D = float((o[idx] * depth).sum() / o[idx].sum())
+        assert out["vis"]["D"][c] == pytest.approx(D, rel=1e-5), c
+        assert out["vis"]["zmin"][c] == pytest.approx(depth.min(), rel=1e-5), c
+        assert out["vis"]["zmax"][c] == pytest.approx(depth.max(), rel=1e-5), c
+        checked += 1
+    assert checked > 0
