@@ -30,8 +30,9 @@
 // Parity pins (tests/test_oracle_*.py): hand cases H1-H12 (tests/golden/), the
 // float64 SPEC-formula brute force B1 (oracle/brute.py), set-level enumeration
 // and the invariants I1-I16 / special cases P1-P6 of SURVEY.md §8(c).
-// D_c (O7) is pinned only by hand case H7 and invariants ("parity partially
-// unpinned" -- see DESIGN.md, ledger L3/L4).
+// D_c (O7) has no paper value: it is pinned by hand case H7, invariants and a
+// float64 recomputation from the caller's extrinsics (tests/test_oracle_props.py;
+// "parity partially pinned" -- see DESIGN.md, ledger L3/L4).
 
 #include <algorithm>
 #include <cmath>
