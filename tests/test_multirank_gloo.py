@@ -94,18 +94,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, cfg=None):
+    cfg = cfg or CFG
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        sc = make_scene(make_config(CFG["base"], G=CFG["G"], N=CFG["N"], seed=CFG["seed"]))
+        sc = make_scene(make_config(cfg["base"], G=cfg["G"], N=cfg["N"], seed=cfg["seed"]))
         eng = Engine(OracleLocal(sc, rank, world))
         m, n = sc.cfg.m, sc.cfg.n
         L = eng.block_loads(m, n)
         A = eng.assign_cameras(m, n)
         c, e = eng.crop_masks(m, n)
-        v = np.array([0.3, 0.55, 0.8], np.float32)
+        v = np.linspace(0.3, 0.8, m - 1).astype(np.float32)
         L2 = eng.block_loads(m, n, v=v)
         q.put((rank, {k: L[k] for k in ("n_cams", "g_vis", "incidences", "g_blk", "objective")},
                {k: A[k] for k in A}, c, e, int(L2["objective"])))
@@ -113,22 +114,25 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_gloo_engine_matches_world1(world):
+TINY = dict(base="tiny", G=3_000, N=17, seed=0xE2)  # 2 x 2 = 4 blocks: with 5 ranks one owns none
+
+
+@pytest.mark.parametrize("world,cfg", [(2, CFG), (3, CFG), (5, CFG), (5, TINY)])
+def test_gloo_engine_matches_world1(world, cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, cfg)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    sc = make_scene(make_config(CFG["base"], G=CFG["G"], N=CFG["N"], seed=CFG["seed"]))
+    sc = make_scene(make_config(cfg["base"], G=cfg["G"], N=cfg["N"], seed=cfg["seed"]))
     ref = oracle.run(sc)
     m, n = sc.cfg.m, sc.cfg.n
-    g2 = oracle.default_grid(m, n, v=np.array([0.3, 0.55, 0.8], np.float32))
+    g2 = oracle.default_grid(m, n, v=np.linspace(0.3, 0.8, m - 1).astype(np.float32))
     ref2 = oracle.evaluate_cuts(sc, ref["pre"], ref["vis"], g2)
     for rank, L, A, c, e, obj2 in res:
         for k in ("n_cams", "g_vis", "incidences", "g_blk"):
