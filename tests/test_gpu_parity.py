@@ -113,6 +113,37 @@ def test_block_masks_group_overflow(groups, monkeypatch):
     full_parity(sc, [_rand_grid(8, 8, 4, tau=0.05), oracle.default_grid(4, 4)])
 
 
+def test_call_orders(tiny_scene):
+    """The evaluation's block counts reach the host asynchronously and the
+    per-camera copies run on a side stream: crop first (device outputs), then
+    loads and assignment, with a second grid evaluated in between, must give
+    the oracle's results for both grids."""
+    import torch
+    lobe = _lobe()
+    sc = tiny_scene
+    g1, g2 = oracle.default_grid(2, 2), _rand_grid(3, 2, 7)
+    o = oracle.run(sc, grid=g1)
+    asg2 = oracle.assign(sc, o["pre"], o["vis"], g2)
+    bl2 = oracle.block_loads(sc, o["pre"], o["vis"], asg2, g2)
+    with lobe.Scene(sc, sc) as S:
+        W64 = (sc.G + 63) // 64
+        cd = torch.empty(4 * W64, dtype=torch.int64, device="cuda")
+        ed = torch.empty(4 * W64, dtype=torch.int64, device="cuda")
+        S.crop_masks_into(2, 2, cd, ed)
+        L2 = S.block_loads(3, 2, **_grid_kw(g2))           # another grid in between
+        L1 = S.block_loads(2, 2)
+        a1 = S.assign_cameras(2, 2)
+        torch.cuda.synchronize()
+        crop = cd.cpu().numpy().view(np.uint64).reshape(4, W64)
+        elig = ed.cpu().numpy().view(np.uint64).reshape(4, W64)
+        a2 = S.assign_cameras(3, 2, **_grid_kw(g2))
+    _cmp_loads(L1, o["loads"])
+    _cmp_loads(L2, bl2)
+    _cmp_percam(a1, o["vis"], o["asg"])
+    _cmp_percam(a2, o["vis"], asg2)
+    assert (crop == o["crop"]).all() and (elig == o["eligible"]).all()
+
+
 def test_mid_size():
     sc = make_scene(make_config("matrixcity", G=150_000, N=120, seed=0x77))
     full_parity(sc, [oracle.default_grid(6, 6), _rand_grid(5, 4, 9)])
