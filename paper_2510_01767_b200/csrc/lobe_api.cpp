@@ -8,6 +8,7 @@
 // -ffp-contract=off: the few fp32 host operations (camera-centre grid
 // coordinates, region bounds) are single IEEE operations in the order written.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -918,6 +919,34 @@ void recycle_pinned_out(uint8_t* p, size_t cap) {
   g_pin_out_free.emplace_back(p, cap);
 }
 
+// Timing events of a scene, recycled across scenes as one set per device.
+std::vector<std::pair<int, std::array<cudaEvent_t, 18>>> g_ev_free;
+void acquire_events(int device, cudaEvent_t (&ev)[18]) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_ev_free.size(); ++i)
+      if (g_ev_free[i].first == device) {
+        for (int k = 0; k < 18; ++k) ev[k] = g_ev_free[i].second[k];
+        g_ev_free.erase(g_ev_free.begin() + i);
+        return;
+      }
+  }
+  for (auto& e : ev) cudaEventCreate(&e);
+}
+void recycle_events(int device, cudaEvent_t (&ev)[18]) {
+  std::array<cudaEvent_t, 18> a;
+  for (int k = 0; k < 18; ++k) {
+    if (!ev[k]) {  // incomplete set: destroy it
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+      return;
+    }
+    a[k] = ev[k];
+  }
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_ev_free.emplace_back(device, a);
+}
+
 // Side streams for the per-camera copies, recycled across scenes (one per
 // live scene; creating a stream costs ~0.4 ms).
 std::vector<std::pair<int, cudaStream_t>> g_side_free;
@@ -1025,8 +1054,7 @@ void lobe_free_scene(lobe_scene* s) {
     cudaStreamSynchronize(s->side);
     recycle_side_stream(s->device, s->side);  // stream creation costs ~0.4 ms: reuse across scenes
   }
-  for (auto& e : s->ev)
-    if (e) cudaEventDestroy(e);
+  recycle_events(s->device, s->ev);  // event creation costs ~2 us each: reuse across scenes
   recycle_pinned(s->pin);
   recycle_pinned_out(s->pin_out, s->pin_out_cap);
   delete s;
@@ -1072,7 +1100,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   s->aniso = (o.predicate == LOBE_PREDICATE_ANISOTROPIC);
   s->frame = F;
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, o.device);
-  for (auto& e : s->ev) cudaEventCreate(&e);
+  acquire_events(o.device, s->ev);
   s->pin = acquire_pinned();
   if (!s->pin) {
     delete s;
