@@ -270,7 +270,13 @@ lobe_status resolve_frame(const lobe_camera* cams, int64_t N, lobe_frame* f) {
   for (int64_t i = 0; i < N; ++i) {
     double o[3];
     cam_centre(cams[i], o);
-    for (int a = 0; a < 3; ++a) c[a][i] = o[a];
+    for (int a = 0; a < 3; ++a) {
+      // the full camera validation runs later; the selections below need
+      // finite centres (a NaN would break their ordering)
+      if (!std::isfinite(o[a]))
+        return fail(LOBE_E_INVALID_INPUT, "camera " + std::to_string(i) + " centre not finite (SPEC.md:46-48)");
+      c[a][i] = o[a];
+    }
   }
   if (f->auto_flags & LOBE_FRAME_AUTO_CENTER) {
     for (int a = 0; a < 3; ++a) {
@@ -1075,7 +1081,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   if (o.assign_mode < 0 || o.assign_mode > 2) return fail(LOBE_E_INVALID_CONFIG, "bad assign_mode");
   if (o.predicate != LOBE_PREDICATE_ISOTROPIC && o.predicate != LOBE_PREDICATE_ANISOTROPIC)
     return fail(LOBE_E_INVALID_CONFIG, "bad predicate");
-  TRY(validate_cameras(cams, n_cams));
+  if (n_cams <= 0) return fail(LOBE_E_INVALID_CONFIG, "n_cams must be > 0 (SPEC.md:110)");
+  // validate_cameras runs later, while the device works on a1 (checked before
+  // the load's first synchronisation); invalid cameras only yield garbage in
+  // that window, never an out-of-range index
   lobe_frame F{};
   if (inout_frame) F = *inout_frame;
   else F.auto_flags = LOBE_FRAME_AUTO_ALL;
@@ -1274,6 +1283,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       cudaFreeAsync(tu, st);
     }
     CK(cudaMemcpyAsync(&s->pin->n_units, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TRY(validate_cameras(cams, n_cams));  // host work overlapping the device's a1 / culling
     CK(cudaStreamSynchronize(st));
     const unsigned long long kept_pairs = s->pin->kept_pairs;
     const uint32_t nu = s->pin->n_units;

@@ -308,6 +308,26 @@ def test_full_size_sampled(name):
                     assert not (rb & ~cb).any()
 
 
+def test_invalid_camera_gpu():
+    """Cameras are validated while the device runs the first kernels of the
+    load; an invalid one still fails the load with INVALID_INPUT (no partial
+    scene) -- non-orthonormal R, z_near >= z_far, a NaN translation."""
+    lobe = _lobe()
+    sc = make_scene("tiny")
+    for field, value in (("R", 1.5), ("z_near", 9.0), ("t", np.nan)):
+        bad = make_scene("tiny")
+        arr = getattr(bad, field)
+        if arr.ndim > 1:
+            arr[7].flat[0] = value
+        else:
+            arr[7] = value
+        with pytest.raises(lobe.LobeError) as e:
+            lobe.Scene(sc, bad)
+        assert e.value.status == "INVALID_INPUT", field
+    with lobe.Scene(sc, sc) as S:  # the valid scene still loads afterwards
+        assert S.assign_cameras(2, 2)["K"].sum() > 0
+
+
 def test_errors_gpu():
     lobe = _lobe()
     g = [dict(mu=[0, 0, 5], s=0.1, o=1.0), dict(mu=[1, 1, 5], s=0.1, o=1.0)]
