@@ -506,11 +506,12 @@ def test_aniso_edge_clusters_exact(seed):
     assert st.dense_tests > 0
 
 
-def test_full_size_sampled_aniso():
-    """The anisotropic mode at MatrixCity size: rows and per-camera outputs of
-    sampled cameras equal the oracle's O6a."""
+@pytest.mark.parametrize("name", ["rubble", "matrixcity"])
+def test_full_size_sampled_aniso(name):
+    """The anisotropic mode at full Rubble and MatrixCity size: rows and
+    per-camera outputs of sampled cameras equal the oracle's O6a."""
     lobe = _lobe()
-    sc = make_scene("matrixcity")
+    sc = make_scene(name)
     m, n = sc.cfg.m, sc.cfg.n
     rng = np.random.default_rng(23)
     sel = np.sort(rng.choice(sc.N, 4, replace=False))

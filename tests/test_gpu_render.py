@@ -60,3 +60,36 @@ def test_clouds_and_assignment(setup):
         L = S.block_loads(g["m"], g["n"], v=g["v"], h=g["h"], delta_v=g["dv"], delta_h=g["dh"], tau=g["tau"])
         for k in ("n_cams", "g_vis", "g_blk", "incidences"):
             assert np.array_equal(L[k], bl[k]), k
+
+
+def test_mid_size_clouds_and_assignment():
+    """A Rubble-shaped scene (40k Gaussians, 12 cameras at 288x216 after the
+    1/4 downscale: many 16x16 tiles, deep splat lists): clouds, assignments
+    and block loads equal the oracle's bit for bit."""
+    import torch
+    from paper_2510_01767_b200 import lobe
+    from synth import make_scene, make_config
+    sc = make_scene(make_config("rubble", G=40_000, N=12, seed=0x4D1))
+    g = oracle.default_grid(3, 3)
+    o = oracle.run(sc, grid=g)
+    cl = oracle.render_clouds(sc, o["pre"], o["vis"], o["frame"])
+
+    class DG:
+        pass
+
+    dg = DG()
+    for k in oracle.SUB_FIELDS:
+        setattr(dg, k, torch.from_numpy(getattr(sc, k)).cuda())
+    with lobe.Scene(sc, sc) as S:
+        S.render_select(dg)
+        off, gu, gv = S.camera_clouds()
+        assert np.array_equal(off, cl["off"])
+        assert np.array_equal(gu, cl["gu"]) and np.array_equal(gv, cl["gv"])
+        ref = oracle.assign_points(sc, o["pre"], cl, g)
+        a = S.assign_cameras(3, 3)
+        assert np.array_equal(a["n"], ref["n"]) and np.array_equal(a["member"], ref["member"])
+        assert np.array_equal(a["home"], ref["home"])
+        bl = oracle.block_loads(sc, o["pre"], o["vis"], ref, g)
+        L = S.block_loads(3, 3)
+        for k in ("n_cams", "g_vis", "g_blk", "incidences"):
+            assert np.array_equal(L[k], bl[k]), k
