@@ -525,3 +525,18 @@ def test_full_size_sampled_aniso(name):
         g = oracle.default_grid(m, n)
         asg = oracle.assign(sc, pre, vis, g)
         _cmp_percam(S.assign_cameras(m, n), vis, asg, sel=sel)
+
+
+def test_dev_vis_bench_variants_identical(tiny_scene):
+    """lobe_dev_vis_bench: every visibility kernel variant (the tile-major
+    production kernel, the culled and dense camera-inner kernels and their
+    other shapes) rewrites the rows with the same bits as the oracle."""
+    lobe = _lobe()
+    o = oracle.run(tiny_scene)
+    with lobe.Scene(tiny_scene, tiny_scene) as S:
+        for variant in range(6):
+            ms, grid = S.dev_vis_bench(variant, reps=1)
+            assert ms > 0 and grid > 0
+            assert (S.export_rows() == o["vis"]["rows"]).all(), variant
+        with pytest.raises(lobe.LobeError):
+            S.dev_vis_bench(99, reps=1)
