@@ -540,3 +540,16 @@ def test_dev_vis_bench_variants_identical(tiny_scene):
             assert (S.export_rows() == o["vis"]["rows"]).all(), variant
         with pytest.raises(lobe.LobeError):
             S.dev_vis_bench(99, reps=1)
+
+
+def test_dev_vis_bench_aniso(tiny_scene):
+    """Anisotropic scenes: the production kernel re-run by lobe_dev_vis_bench
+    keeps the O6a rows; the camera-inner variants are isotropic only."""
+    lobe = _lobe()
+    o = oracle.run(tiny_scene, predicate=oracle.PRED_ANISO)
+    with lobe.Scene(tiny_scene, tiny_scene, predicate=1) as S:
+        S.dev_vis_bench(0, reps=2)
+        assert (S.export_rows() == o["vis"]["rows"]).all()
+        with pytest.raises(lobe.LobeError) as e:
+            S.dev_vis_bench(1, reps=1)
+        assert e.value.status == "INVALID_CONFIG"
