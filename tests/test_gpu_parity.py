@@ -486,6 +486,15 @@ def test_aniso_tiny_full(tiny_scene):
     full_parity(tiny_scene, [oracle.default_grid(2, 2), _rand_grid(3, 3, 5)], predicate=1)
 
 
+def test_aniso_ieee_path():
+    """A camera with z_far beyond 2^126 disables the branch-free reciprocal /
+    square roots for the scene (host check): the IEEE kernel variant must give
+    the same O6a results."""
+    sc = make_scene("tiny")
+    sc.z_far[3] = np.float32(1e38)
+    full_parity(sc, [oracle.default_grid(2, 2)], predicate=1)
+
+
 def test_aniso_ragged():
     from synth.scenes import make_config, make_scene
     sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x2510AA01))
