@@ -172,6 +172,25 @@ def test_hand_depth_H7_gpu():
         assert a["zmin"][0] == d["z_min"] and a["zmax"][0] == d["z_max"]
 
 
+@pytest.mark.parametrize("case", GOLD["frame_auto"]["cases"], ids=[c["id"] for c in GOLD["frame_auto"]["cases"]])
+def test_hand_frame_auto_gpu(case):
+    """O2 automatic frame resolved by lobe_load_scene equals the hand-worked
+    centre and radius (tests/golden/hand_cases.json frame_auto)."""
+    from tests.test_oracle_hand import frame_cameras, FRAME_GAUSSIANS
+    lobe = _lobe()
+    extra = "extra_identity_camera_t" in case
+    sc = mini_scene(FRAME_GAUSSIANS, frame_cameras(case, extra=extra))
+    with lobe.Scene(sc, sc) as S:
+        assert list(S.frame["center"]) == [np.float32(v) for v in case["center"]], case["why"]
+        assert S.frame["radius"] == np.float32(case["radius"]), case["why"]
+        assert list(S.frame["axis_u"]) == [1, 0, 0] and list(S.frame["axis_v"]) == [0, 1, 0]
+    if extra:
+        sc0 = mini_scene(FRAME_GAUSSIANS, frame_cameras(case))
+        with pytest.raises(lobe.LobeError) as e:
+            lobe.Scene(sc0, sc0)
+        assert e.value.code == 5  # LOBE_E_DEGENERATE_SCENE
+
+
 def test_hand_assignment_H9_gpu():
     lobe = _lobe()
     a = GOLD["assignment"]

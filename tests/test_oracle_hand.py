@@ -247,3 +247,57 @@ def test_errors():
     with pytest.raises(oracle.OracleError) as e:
         oracle.assign(sc, pre, vis, grid)
     assert e.value.status == "INVALID_CUTS"
+
+
+# ------------------------------------------------------------------ O2 frame
+FRAME = GOLD["frame_auto"]
+
+
+def frame_cameras(case, extra=False):
+    """Cameras of a frame case: identity R with t = -o (so o = -R^T t = the listed
+    centre), or the case's rotated pose; F3 optionally adds its identity camera."""
+    cams = []
+    for o in case["centers"]:
+        c = dict(fx=100.0, fy=100.0, cx=50.0, cy=50.0, width=100, height=100, z_near=0.1, z_far=100.0)
+        if "rotated" in case:
+            c["R"] = np.asarray(case["rotated"]["R"], float)
+            c["t"] = np.asarray(case["rotated"]["t"], float)
+        else:
+            c["R"] = np.eye(3)
+            c["t"] = -np.asarray(o, float)
+        cams.append(c)
+    if extra:
+        cams.append(dict(fx=100.0, fy=100.0, cx=50.0, cy=50.0, width=100, height=100, z_near=0.1, z_far=100.0,
+                         R=np.eye(3), t=np.asarray(case["extra_identity_camera_t"], float)))
+    return cams
+
+
+FRAME_GAUSSIANS = [dict(mu=[-1, -1, 0], s=0.01, o=0.5), dict(mu=[1, 1, 0.5], s=0.01, o=0.5)]
+
+
+@pytest.mark.parametrize("case", FRAME["cases"], ids=[c["id"] for c in FRAME["cases"]])
+def test_frame_auto_hand_case(case):
+    extra = "extra_identity_camera_t" in case
+    sc = mini_scene(FRAME_GAUSSIANS, frame_cameras(case, extra=extra))
+    c0, rho, au, av = oracle.frame(sc)
+    assert list(c0) == [np.float32(v) for v in case["center"]], (case["id"], case["why"])
+    assert rho == np.float32(case["radius"]), (case["id"], case["why"])
+    assert list(au) == [1, 0, 0] and list(av) == [0, 1, 0]
+    if extra:  # without the extra camera every distance is 0: DEGENERATE_SCENE (SPEC.md:80)
+        assert case["radius_without_extra"] == 0
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.frame(mini_scene(FRAME_GAUSSIANS, frame_cameras(case)))
+        assert e.value.status == "DEGENERATE_SCENE"
+
+
+def test_frame_auto_overrides():
+    """Caller values override each default independently (O2 'Caller-supplied
+    values override the defaults'): a given centre changes the radius's
+    reference point (F1 about (0,0,0): distances 3,sqrt(41),sqrt(80),sqrt(13),0,
+    sqrt(221) -> 6th = sqrt(221))."""
+    case = FRAME["cases"][0]
+    sc = mini_scene(FRAME_GAUSSIANS, frame_cameras(case))
+    c0, rho, _, _ = oracle.frame(sc, center=[0, 0, 0])
+    assert list(c0) == [0, 0, 0] and rho == np.float32(np.sqrt(221.0))
+    c0, rho, _, _ = oracle.frame(sc, radius=7.5)
+    assert list(c0) == [2, 0, 0] and rho == np.float32(7.5)
