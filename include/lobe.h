@@ -23,19 +23,26 @@
  *     is released by lobe_free_scene.
  *   - Pointers: output (and, with on_device, input) pointers may be host or
  *     device pointers (unified addressing decides); device writes are issued on
- *     lobe_options.stream and every call returns after that stream has drained.
+ *     lobe_options.stream. Host outputs are complete when a call returns; device
+ *     outputs of lobe_crop_masks are stream-ordered (the call returns without
+ *     waiting, like a kernel launch), every other call's outputs are complete on
+ *     return.
  *   - Index conventions: Gaussian i is the caller's index; camera c is the
  *     caller's array index. Block b = p*n + q (0-based), p indexes the v cuts
  *     (first ground axis), q the h cuts (PAPER.md:165 garbled index read as
  *     b = (i-1) n + j, ledger L9). B = m*n <= 64. Mask bit (i mod 64) of u64 word
  *     floor(i/64) is Gaussian i.
- *   - Multi-GPU: options.rank / options.world select this process's camera shard
- *     [floor(rN/W), floor((r+1)N/W)) (cameras sharded, Gaussians replicated).
- *     Per-camera outputs of the calls below cover the LOCAL shard; block-level
- *     calls that need the other ranks' cameras take the exchanged partials through
- *     the lobe_*_partial / lobe_*_combine calls; the Python layer
- *     (paper_2510_01767_b200/engine.py) drives the exchange over torch.distributed
- *     (NCCL). With world == 1 every call is complete on its own.
+ *   - Multi-GPU: options.rank / options.world select this
+ *     process's camera shard [floor(rN/W), floor((r+1)N/W)) (cameras sharded,
+ *     Gaussians replicated). With a communicator (options.nccl_unique_id or
+ *     options.host_comm) ALL ranks call every function collectively (MPI style,
+ *     same arguments), the library runs the exchange itself (NCCL on the scene's
+ *     stream, or the caller's host callbacks), and every output is GLOBAL and
+ *     identical on every rank: per-camera outputs cover all N cameras. Without a
+ *     communicator and world > 1 the scene is a bare camera shard: per-camera
+ *     outputs cover the local shard and the block-level results come from the
+ *     exchange points below (lobe_block_partial, lobe_masks_combine, ...).
+ *     With world == 1 and no communicator every call is complete on its own.
  *   - Concurrency: a handle is not thread-safe; distinct handles are. Every call
  *     is deterministic (identical inputs give identical bytes, for any world).
  */
@@ -57,7 +64,7 @@ typedef enum {
   LOBE_E_INVALID_INDEX = 4,     /* bad block / camera index */
   LOBE_E_DEGENERATE_SCENE = 5,  /* all points identical on a ground axis, zero radius */
   LOBE_E_CUDA = 6,              /* CUDA runtime error or no device */
-  LOBE_E_NCCL = 7,              /* reserved: collective failure reported by the exchange layer */
+  LOBE_E_NCCL = 7,              /* collective failure: NCCL error / library missing, or a host_comm callback failed */
   LOBE_E_OOM = 8,               /* device allocation failed */
   LOBE_E_STATE = 9,             /* call out of order (e.g. combine before partial) */
   LOBE_E_CAPACITY = 10,         /* output capacity too small (the needed count is reported) */
@@ -109,13 +116,41 @@ typedef struct {
 #define LOBE_ASSIGN_HOME 1
 #define LOBE_ASSIGN_UNION 2
 
+/* Caller-provided collectives over HOST buffers (any transport: gloo, MPI, ...).
+ * Each returns 0 on success; every rank calls them in the same order.
+ *   all_gather: recv (world x bytes, rank-major) = every rank's `bytes` of send;
+ *   all_reduce_u64: element-wise SUM over ranks, in place;
+ *   all_to_all_v: send_bytes[j] bytes at send + send_off[j] go to rank j; the
+ *     recv_bytes[j] bytes from rank j land at recv + recv_off[j]. */
+typedef struct {
+  void* ctx;
+  int (*all_gather)(void* ctx, const void* send, void* recv, size_t bytes);
+  int (*all_reduce_u64)(void* ctx, uint64_t* buf, size_t count);
+  int (*all_to_all_v)(void* ctx, const void* send, const size_t* send_bytes, const size_t* send_off, void* recv,
+                      const size_t* recv_bytes, const size_t* recv_off);
+} lobe_host_comm;
+
 typedef struct {
   int32_t device;       /* CUDA device ordinal */
   int32_t rank, world;  /* camera shard; world >= 1 */
   void* stream;         /* cudaStream_t; NULL = legacy default stream */
   int32_t assign_mode;  /* LOBE_ASSIGN_* */
   int32_t predicate;    /* LOBE_PREDICATE_* (0 = isotropic, the default) */
+  /* Communicator; at most one, both NULL = none.
+   * nccl_unique_id: 128 bytes (an ncclUniqueId from lobe_nccl_unique_id on rank 0,
+   *   broadcast by the caller); the library creates one ncclComm per (id, rank,
+   *   device) on first use -- collectively, so every rank must load its scene --
+   *   and reuses it for later scenes with the same id (lobe_release_comms frees).
+   * host_comm: host collectives (copied; must outlive the scene's calls). */
+  const void* nccl_unique_id;
+  const lobe_host_comm* host_comm;
 } lobe_options;
+
+/* NCCL unique id for options.nccl_unique_id (rank 0 calls this and broadcasts the
+ * 128 bytes). LOBE_E_NCCL if libnccl.so.2 cannot be loaded. Needs no scene. */
+lobe_status lobe_nccl_unique_id(void* out_128_bytes);
+/* Destroy the cached NCCL communicators (collective over each communicator). */
+void lobe_release_comms(void);
 
 /* Visibility predicate. ISOTROPIC: SPEC.md:299's culling bound, footprint radius
  * 3 max(s) max(fx, fy) / z (the measured path). ANISOTROPIC: the
@@ -162,8 +197,9 @@ typedef struct {
 } lobe_balance_opts;
 
 /* Stage timings of the last call (CUDA events on options.stream), cumulative
- * logical Gaussian-camera tests executed by the visibility kernel (I16), and
- * algorithmic bytes of the last visibility pass. */
+ * logical Gaussian-camera tests decided by the visibility kernels (I16: counted
+ * inside k_cull / k_vis_tiles, see decided_tests), and algorithmic bytes of the
+ * last visibility pass. */
 typedef struct {
   double t_prep_ms, t_vis_ms, t_hist_ms, t_loads_ms, t_comm_ms, t_crop_ms;
   uint64_t tests_executed, bytes_read, bytes_written;
@@ -183,6 +219,16 @@ typedef struct {
   uint64_t accepted_tests;  /* tests in (slice, camera) pairs the slice bound accepted (last pass) */
   uint64_t exact_variant_tests[6]; /* exact tests by the conditions left open: left edge only, top edge only,
                                       right edge only, bottom edge only, the four edges, all six */
+  uint64_t decided_tests[4]; /* I16, measured by the kernels of the last visibility pass: the logical
+                                tests over REAL Gaussians (padding excluded) decided by [0] the chunk / tile bound
+                                (k_cull, rejected), [1] the slice bound rejecting, [2] the slice bound accepting,
+                                [3] the exact per-Gaussian test; they add up to G x N_local when every pair is
+                                decided exactly once. tests_executed accumulates their sum over loads. */
+  uint64_t visible_bits[2];  /* visible (Gaussian, camera) bits written by the last pass for accepted / exact-tested
+                                slices; their sum equals sum_c K_c of the local cameras */
+  uint64_t exact_pattern_tests[9]; /* isotropic exact tests by open-condition pattern (k_vis_tiles): left, top,
+                                      right, bottom edge; top-left, top-right, bottom-left corner; the four edges;
+                                      all six -- 3, 3, 7, 7, 6, 10, 10, 11, 11 FFMA per test (issued flop) */
 } lobe_stats;
 
 /* ---- scene --------------------------------------------------------------- */
@@ -198,10 +244,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* gaussians, const lobe_camera* 
 void lobe_free_scene(lobe_scene* scene);
 const char* lobe_last_error(void);
 
-/* ---- per-camera outputs (local shard: n_local entries, see lobe_get_stats) -- */
+/* ---- per-camera outputs: N entries (global) with a communicator or world == 1;
+ *      a bare shard's n_local entries (see lobe_scene_info) otherwise -------- */
 
 /* K_c, depth mean D_c = sum(o w)/sum(o) over V_c (0 if K_c = 0, ledger L4/L7),
- * z_min/z_max over V_c (+inf/-inf if K_c = 0); n_cb/n0_cb: n_local x B counts of
+ * z_min/z_max over V_c (+inf/-inf if K_c = 0); n_cb/n0_cb: N x B counts of
  * V_c inside the enlarged regions / delta = 0 cells;
  * member: bit b set iff K_c > 0 and n_cb >= tau K_c;
  * home: lowest b maximising n0_cb, camera-centre cell if K_c = 0 (ledger L7/L8).
@@ -212,7 +259,7 @@ lobe_status lobe_assign_cameras(lobe_scene* scene, const lobe_grid* grid, uint32
                                 float* z_min, float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member,
                                 int32_t* home);
 
-/* ---- block loads (world == 1: complete) ---------------------------------- */
+/* ---- block loads (world == 1 or with a communicator: complete) ---------- */
 
 /* out: B records; objective: max_b g_vis. */
 lobe_status lobe_block_loads(lobe_scene* scene, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective);
@@ -230,8 +277,10 @@ lobe_status lobe_crop_masks(lobe_scene* scene, const lobe_grid* grid, uint64_t* 
  * evaluations in total, each cut bounded to move at most halfway to its
  * neighbours. v_out: m-1, h_out: n-1 floats; history: L objective values
  * (may be NULL); cut_history: L x (m+n-2) floats (may be NULL); best: B records
- * at the returned cuts (may be NULL). world == 1 only; multi-rank runs use
- * lobe_bo_run with the exchange layer's objective. */
+ * at the returned cuts (may be NULL). With a communicator every evaluation is a
+ * collective exchange; the deterministic BO then proposes the same cuts on every
+ * rank (identical objective values), so no broadcast is needed. A bare shard
+ * (world > 1, no communicator) returns LOBE_E_STATE. */
 lobe_status lobe_balance_partition(lobe_scene* scene, int32_t m, int32_t n, const lobe_balance_opts* opts,
                                    float* v_out, float* h_out, uint32_t* history, float* cut_history,
                                    lobe_block_load* best);
@@ -242,7 +291,7 @@ typedef int (*lobe_objective_fn)(void* ctx, const float* v, const float* h, uint
 lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lobe_objective_fn objective, void* ctx,
                         float* v_out, float* h_out, uint32_t* history, float* cut_history);
 
-/* ---- multi-rank exchange points (used by engine.py when world > 1) ------- */
+/* ---- multi-rank exchange points (bare shards: world > 1 without a communicator) */
 
 /* Rank-local part of lobe_block_loads: d_masks (DEVICE, B x lobe_mask_words
  * u32, internal Gaussian order) receives OR over the LOCAL cameras of C^(b);
@@ -262,6 +311,21 @@ lobe_status lobe_block_records(lobe_scene* scene, const lobe_grid* grid, const u
 /* Crop / eligible masks (caller order) from combined masks d_masks (DEVICE). */
 lobe_status lobe_crop_from_masks(lobe_scene* scene, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
                                  uint64_t* eligible);
+
+/* The exchange of SURVEY §8(e) on HOST buffers with host collectives (no GPU):
+ * the same choreography the collective calls run (lib-internal xchg_*), exported
+ * so a CPU process group can drive it (tests: gloo with oracle partials).
+ * block loads: partial B x words u32, counts_local 2B u64 [|C^(b)| | I_b] ->
+ *   own (this rank's blocks [floor(rB/W), floor((r+1)B/W)) x words, the OR of all
+ *   ranks' partials), g_vis (B), counts_global (2B);
+ * all masks: own -> all (B x words); gather cameras: N entries of elem bytes. */
+lobe_status lobe_xchg_block_loads_host(const lobe_host_comm* comm, int32_t rank, int32_t world, int32_t B,
+                                       size_t words, const uint32_t* partial, const uint64_t* counts_local,
+                                       uint32_t* own, uint32_t* g_vis, uint64_t* counts_global);
+lobe_status lobe_xchg_all_masks_host(const lobe_host_comm* comm, int32_t rank, int32_t world, int32_t B, size_t words,
+                                     const uint32_t* own, uint32_t* all);
+lobe_status lobe_xchg_gather_cameras_host(const lobe_host_comm* comm, int32_t rank, int32_t world, int64_t N,
+                                          size_t elem, const void* local, void* out);
 
 /* ---- introspection / tests ----------------------------------------------- */
 

@@ -17,8 +17,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["lobe_kernels.cu"]
-SOURCES_CPP = ["lobe_api.cpp", "lobe_bo.cpp"]
-HEADERS = ["lobe_internal.h", os.path.join("..", "..", "include", "lobe.h")]
+SOURCES_CPP = ["lobe_api.cpp", "lobe_bo.cpp", "lobe_comm.cpp"]
+HEADERS = ["lobe_internal.h", "lobe_comm.h", os.path.join("..", "..", "include", "lobe.h")]
 
 
 def _newer(target, deps):
@@ -55,7 +55,7 @@ def build(force=False, verbose_ptxas=False):
                   "-Wno-unused-function", "-I", CUDA_INC, "-c", s, "-o", o])
         objs.append(o)
     if force or _newer(OUT, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs])
+        _run([NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-ldl"])
         os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -26,6 +26,7 @@
 
 #include "../../include/lobe.h"
 #include "lobe_internal.h"
+#include "lobe_comm.h"
 
 using namespace lobe;
 
@@ -107,6 +108,8 @@ struct DevBuf {
 
 }  // namespace
 
+constexpr int kNumEvents = 20;
+
 struct lobe_scene {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -184,7 +187,7 @@ struct lobe_scene {
     uint8_t zp_cell[kMaxZones * kMaxZones];
     alignas(16) uint32_t counts[3 * kMaxBlocks];  // mirrors the device block: ncams, gvis, gblk
     unsigned long long incid[kMaxBlocks];   // then incid (contiguous on the device too)
-    unsigned long long vc[8];               // k_vis_tiles counters of the last pass
+    unsigned long long vc[32];              // k_vis_tiles / k_cull counters of the last pass (VisArgs::counters)
     uint32_t prep_hs[8];                    // k_prep_raw: error flags, ordered ground min / max
     uint32_t n_pairs;                       // non-empty (tile, camera) pairs of the last load
     uint32_t n_units;                       // visibility work units of the last load
@@ -216,7 +219,18 @@ struct lobe_scene {
   const unsigned long long* h_incid() { wait_counts(); return pin->incid; }
   // stats
   lobe_stats st{};
-  cudaEvent_t ev[18] = {};  // load pass: 0, 1, 8-12, 16, 17; evaluation: 2-4, 13; comm: 5, 6; dev bench: 6, 7; crop: 14, 15
+  cudaEvent_t ev[kNumEvents] = {};  // load pass: 0, 1, 8-12, 16, 17; evaluation: 2-4, 13; combine: 5, 6; dev bench:
+                                    // 6, 7; crop: 14, 15; collective exchange: 18, 19
+  // ---- communicator: collective calls, global outputs
+  lobe::Comm* comm = nullptr;
+  lobe::XOps* xops = nullptr;       // device-memory ops of comm on `stream`
+  uint32_t* own_masks = nullptr;    // combined masks of this rank's blocks (last exchange)
+  int own_cap = 0;                  // blocks own_masks can hold
+  unsigned long long* d_xcounts = nullptr;  // [2 x kMaxBlocks] u64: |C^(b)| then I_b
+  uint32_t x_gvis[kMaxBlocks] = {};         // global G_vis of the last exchange
+  uint64_t x_counts[2 * kMaxBlocks] = {};   // global |C^(b)|, I_b of the last exchange
+  bool x_valid = false;                     // the cached evaluation has been exchanged
+  bool x_all = false;                       // `masks` holds every block's combined masks
 
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -462,6 +476,8 @@ float ms_between(cudaEvent_t a, cudaEvent_t b) {
 lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   cudaStream_t st = s->stream;
   s->wait_counts();  // the previous evaluation's copies read / write `pin`
+  s->x_valid = false;
+  s->x_all = false;
   // ---- a5 zone tables (host) + per-Gaussian zones (device)
   ZoneTables Z{};
   build_axis(g.m, g.v, g.dv, &Z.U);
@@ -550,6 +566,49 @@ lobe_status ensure_eval(lobe_scene* s, const GridV& g) {
   s->ev_dh = g.dh;
   s->ev_tau = g.tau;
   s->ev_mode = s->assign_mode;
+  return LOBE_OK;
+}
+
+// With a communicator: the evaluation of this grid on the local cameras (partial
+// masks in s->masks, local counts), then the collective exchange of SURVEY §8e
+// (lobe_comm.h): every rank ends with the global G_vis, |C^(b)|, I_b and the
+// combined masks of its own blocks. One host round trip (the B G_vis values and
+// 2B counts); cached with the evaluation.
+lobe_status ensure_xchg(lobe_scene* s, const GridV& g) {
+  TRY(ensure_eval(s, g));
+  if (s->x_valid) return LOBE_OK;
+  const int B = g.B, W = s->world, r = s->rank;
+  const int nb = (int)(lobe::shard_begin(B, r + 1, W) - lobe::shard_begin(B, r, W));
+  if (s->own_cap < nb) {
+    s->release(s->own_masks);
+    CK(s->alloc(&s->own_masks, (size_t)std::max(nb, 1) * s->words));
+    s->own_cap = nb;
+  }
+  // local |C^(b)| (u32 -> u64) and I_b into the exchange buffer, on the device
+  KL(launch_xcounts(s->counts, s->incid, B, s->d_xcounts, s->stream));
+  CK(cudaEventRecord(s->ev[18], s->stream));
+  lobe_status xs = lobe::xchg_block_loads(*s->xops, r, W, B, (size_t)s->words, s->masks,
+                                          reinterpret_cast<uint64_t*>(s->d_xcounts), s->own_masks, s->x_gvis,
+                                          s->x_counts);
+  if (xs != LOBE_OK) return fail(xs, "exchange: " + s->xops->err);
+  CK(cudaEventRecord(s->ev[19], s->stream));
+  CK(cudaEventSynchronize(s->ev[19]));
+  s->st.t_comm_ms = ms_between(s->ev[18], s->ev[19]);
+  s->x_valid = true;
+  return LOBE_OK;
+}
+
+// ... and every block's combined masks in s->masks (for the crop)
+lobe_status ensure_xchg_masks(lobe_scene* s, const GridV& g) {
+  TRY(ensure_xchg(s, g));
+  if (s->x_all) return LOBE_OK;
+  CK(cudaEventRecord(s->ev[18], s->stream));
+  lobe_status xs = lobe::xchg_all_masks(*s->xops, s->rank, s->world, g.B, (size_t)s->words, s->own_masks, s->masks);
+  if (xs != LOBE_OK) return fail(xs, "exchange: " + s->xops->err);
+  CK(cudaEventRecord(s->ev[19], s->stream));
+  CK(cudaEventSynchronize(s->ev[19]));
+  s->st.t_comm_ms += ms_between(s->ev[18], s->ev[19]);
+  s->x_all = true;
   return LOBE_OK;
 }
 
@@ -877,7 +936,17 @@ void finalize_load_stats(lobe_scene* s) {
   s->st.kept_tests = (uint64_t)s->kept_pairs_last * (uint64_t)kTile;  // pairs surviving the tile bound
   s->st.dense_tests = (uint64_t)s->pin->vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
   s->st.accepted_tests = (uint64_t)s->pin->vc[1] * (uint64_t)(kTile / 4);
-  for (int v = 0; v < 6; ++v) s->st.exact_variant_tests[v] = (uint64_t)s->pin->vc[2 + v] * (uint64_t)(kTile / 4);
+  for (int p = 0; p < 9; ++p) s->st.exact_pattern_tests[p] = (uint64_t)s->pin->vc[16 + p] * (uint64_t)(kTile / 4);
+  for (int v = 0; v < 4; ++v) s->st.exact_variant_tests[v] = s->st.exact_pattern_tests[v];
+  s->st.exact_variant_tests[4] = s->st.exact_pattern_tests[4] + s->st.exact_pattern_tests[5] +
+                                 s->st.exact_pattern_tests[6] + s->st.exact_pattern_tests[7];
+  s->st.exact_variant_tests[5] = s->st.exact_pattern_tests[8];
+  // I16, counted by k_cull / k_vis_tiles themselves (VisArgs::counters [8..13])
+  uint64_t decided = 0;
+  for (int k = 0; k < 4; ++k) decided += (s->st.decided_tests[k] = (uint64_t)s->pin->vc[8 + k]);
+  s->st.visible_bits[0] = (uint64_t)s->pin->vc[12];
+  s->st.visible_bits[1] = (uint64_t)s->pin->vc[13];
+  s->st.tests_executed += decided;
   s->stats_pending = false;
 }
 
@@ -926,22 +995,22 @@ void recycle_pinned_out(uint8_t* p, size_t cap) {
 }
 
 // Timing events of a scene, recycled across scenes as one set per device.
-std::vector<std::pair<int, std::array<cudaEvent_t, 18>>> g_ev_free;
-void acquire_events(int device, cudaEvent_t (&ev)[18]) {
+std::vector<std::pair<int, std::array<cudaEvent_t, kNumEvents>>> g_ev_free;
+void acquire_events(int device, cudaEvent_t (&ev)[kNumEvents]) {
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
     for (size_t i = 0; i < g_ev_free.size(); ++i)
       if (g_ev_free[i].first == device) {
-        for (int k = 0; k < 18; ++k) ev[k] = g_ev_free[i].second[k];
+        for (int k = 0; k < kNumEvents; ++k) ev[k] = g_ev_free[i].second[k];
         g_ev_free.erase(g_ev_free.begin() + i);
         return;
       }
   }
   for (auto& e : ev) cudaEventCreate(&e);
 }
-void recycle_events(int device, cudaEvent_t (&ev)[18]) {
-  std::array<cudaEvent_t, 18> a;
-  for (int k = 0; k < 18; ++k) {
+void recycle_events(int device, cudaEvent_t (&ev)[kNumEvents]) {
+  std::array<cudaEvent_t, kNumEvents> a;
+  for (int k = 0; k < kNumEvents; ++k) {
     if (!ev[k]) {  // incomplete set: destroy it
       for (auto& e : ev)
         if (e) cudaEventDestroy(e);
@@ -994,7 +1063,7 @@ lobe_status stage_out(lobe_scene* s, std::vector<StagedCopy>& plan, size_t& used
   return LOBE_OK;
 }
 lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used,
-                       const std::vector<const void*>& srcs) {
+                       const std::vector<const void*>& srcs, cudaEvent_t after = nullptr) {
   if (plan.empty()) {
     CK(cudaStreamSynchronize(s->stream));
     return LOBE_OK;
@@ -1014,7 +1083,7 @@ lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used
       return fail(LOBE_E_CUDA, "pinned staging allocation failed");
     }
   }
-  CK(cudaStreamWaitEvent(s->side, s->ev[4], 0));
+  CK(cudaStreamWaitEvent(s->side, after ? after : s->ev[4], 0));
   for (size_t i = 0; i < plan.size(); ++i)
     CK(cudaMemcpyAsync(s->pin_out + plan[i].off, srcs[i], plan[i].bytes, cudaMemcpyDeviceToHost, s->side));
   CK(cudaStreamSynchronize(s->side));
@@ -1055,7 +1124,10 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
   s->release(s->ncb); s->release(s->n0cb); s->release(s->member); s->release(s->sel); s->release(s->home);
   s->release(s->counts); s->incid = nullptr; s->release(s->masks);
+  s->release(s->own_masks); s->release(s->d_xcounts);
   cudaStreamSynchronize(s->stream);
+  delete s->xops;
+  lobe::comm_release_scene(s->comm);
   if (s->side) {
     cudaStreamSynchronize(s->side);
     recycle_side_stream(s->device, s->side);  // stream creation costs ~0.4 ms: reuse across scenes
@@ -1117,6 +1189,15 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   }
   lobe_status rs = [&]() -> lobe_status {
     cudaStream_t st = s->stream;
+    {  // communicator first: NCCL creation is collective (every rank is in this call)
+      std::string cerr;
+      const lobe_status cs = lobe::comm_acquire(o, &s->comm, &cerr);
+      if (cs != LOBE_OK) return fail(cs, cerr);
+      if (s->comm) {
+        s->xops = lobe::comm_device_ops(s->comm, o.device, st);
+        CK(s->alloc(&s->d_xcounts, 2 * kMaxBlocks));
+      }
+    }
     const int64_t G = g->n;
     s->G = G;
     s->G_pad = (G + kChunk - 1) / kChunk * kChunk;
@@ -1236,7 +1317,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->tile_hi, (size_t)s->n_tiles));
     CK(s->alloc(&s->slice_lo, (size_t)s->n_tiles * 4));
     CK(s->alloc(&s->slice_hi, (size_t)s->n_tiles * 4));
-    CK(s->alloc(&s->vcnt, 8));
+    CK(s->alloc(&s->vcnt, 32));
     CK(s->alloc(&s->chunk_lo, (size_t)s->n_chunks));
     CK(s->alloc(&s->chunk_hi, (size_t)s->n_chunks));
     CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
@@ -1248,7 +1329,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
-    if (s->N_loc > 0) KLN(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, s->cams, s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, st), 2);
+    CK(cudaMemsetAsync(s->vcnt, 0, 32 * sizeof(unsigned long long), st));
+    if (s->N_loc > 0)
+      KLN(launch_cull(s->tile_lo, s->tile_hi, s->chunk_lo, s->chunk_hi, s->n_tiles, G, s->cams,
+                      s->aniso ? s->acams : nullptr, s->N_loc, s->keep, s->kept, s->vcnt + 8, st), 2);
     CK(cudaEventRecord(s->ev[8], st));
     // kept-camera lists per tile (CSR)
     // list sizes go to pinned memory: the copies do not block the host, which
@@ -1326,7 +1410,6 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     s->release(uc);
     s->release(uoff);
-    CK(cudaMemsetAsync(s->vcnt, 0, 8 * sizeof(unsigned long long), st));
     CK(cudaEventRecord(s->ev[9], st));
     if (s->N_loc > 0 && kept_pairs > 0) {
       VisArgs va{};
@@ -1345,6 +1428,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.slo = s->slice_lo;
       va.shi = s->slice_hi;
       va.counters = s->vcnt;
+      va.G = G;
       va.aniso = s->aniso;
       va.cv = s->cv;
       va.acams = s->acams;
@@ -1432,7 +1516,6 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // enqueues the next call; event timings are read lazily (finalize_load_stats)
     s->kept_pairs_last = kept_pairs;
     s->stats_pending = true;
-    s->st.tests_executed += (uint64_t)G * (uint64_t)s->N_loc;
     s->st.vis_launches += s->N_loc > 0 ? 1 : 0;
     s->st.bytes_read = (uint64_t)s->G_pad * 16ull;
     s->st.bytes_written = (uint64_t)s->N_loc * (uint64_t)s->words * 4ull;
@@ -1473,16 +1556,37 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
     else if (dst && bytes) direct = true;
     return LOBE_OK;
   };
-  TRY(add(K, s->K, NL * 4));
-  TRY(add(depth_mean, s->D, NL * 8));
-  TRY(add(z_min, s->zmin, NL * 4));
-  TRY(add(z_max, s->zmax, NL * 4));
   // device layout of n, n0 is [c][B] with B = g.B stride
-  TRY(add(n_cb, s->ncb, NL * g.B * 4));
-  TRY(add(n0_cb, s->n0cb, NL * g.B * 4));
-  TRY(add(member, s->member, NL * 8));
-  TRY(add(home, s->home, NL * 4));
-  TRY(run_staged(s, plan, used, srcs));
+  struct Arr {
+    void* dst;
+    const void* src;
+    size_t elem;
+  };
+  const Arr arrs[8] = {{K, s->K, 4},           {depth_mean, s->D, 8},   {z_min, s->zmin, 4},
+                       {z_max, s->zmax, 4},    {n_cb, s->ncb, 4 * (size_t)g.B}, {n0_cb, s->n0cb, 4 * (size_t)g.B},
+                       {member, s->member, 8}, {home, s->home, 4}};
+  std::vector<uint8_t*> gathered;
+  if (s->comm) {  // collective: every rank receives all N cameras
+    const int64_t N = s->N_all;
+    CK(cudaEventRecord(s->ev[18], s->stream));
+    for (const Arr& a : arrs) {
+      if (!a.dst) continue;
+      uint8_t* gb = nullptr;
+      CK(s->alloc(&gb, (size_t)N * a.elem));
+      gathered.push_back(gb);
+      lobe_status xs = lobe::xchg_gather_cameras(*s->xops, s->rank, s->world, N, a.elem, a.src, gb);
+      if (xs != LOBE_OK) {
+        for (uint8_t* p : gathered) s->release(p);
+        return fail(xs, "exchange: " + s->xops->err);
+      }
+      TRY(add(a.dst, gb, (size_t)N * a.elem));
+    }
+    CK(cudaEventRecord(s->ev[19], s->stream));
+  } else {
+    for (const Arr& a : arrs) TRY(add(a.dst, a.src, NL * a.elem));
+  }
+  TRY(run_staged(s, plan, used, srcs, s->comm ? s->ev[19] : nullptr));
+  for (uint8_t* p : gathered) s->release(p);
   if (direct) CK(cudaStreamSynchronize(s->stream));  // outputs are complete on return
   return LOBE_OK;
 }
@@ -1490,10 +1594,18 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
 lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
-  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_block_partial + lobe_masks_combine");
+  if (s->world != 1 && !s->comm)
+    return fail(LOBE_E_STATE, "bare shard (world > 1, no communicator): use lobe_block_partial + lobe_masks_combine");
   CK(cudaSetDevice(s->device));
   GridV g;
   TRY(check_grid(grid, &g));
+  if (s->comm) {
+    TRY(ensure_xchg(s, g));
+    uint32_t nc[kMaxBlocks];
+    for (int b = 0; b < g.B; ++b) nc[b] = (uint32_t)s->x_counts[b];
+    fill_records(s, g, nc, s->x_counts + g.B, s->x_gvis, out, objective);
+    return LOBE_OK;
+  }
   TRY(ensure_eval(s, g));
   uint64_t inc[kMaxBlocks];
   for (int b = 0; b < g.B; ++b) inc[b] = s->h_incid()[b];
@@ -1504,11 +1616,15 @@ lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_lo
 lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
-  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_crop_from_masks on combined masks");
+  if (s->world != 1 && !s->comm)
+    return fail(LOBE_E_STATE, "bare shard (world > 1, no communicator): use lobe_crop_from_masks on combined masks");
   CK(cudaSetDevice(s->device));
   GridV g;
   TRY(check_grid(grid, &g));
-  TRY(ensure_eval(s, g));
+  if (s->comm)
+    TRY(ensure_xchg_masks(s, g));
+  else
+    TRY(ensure_eval(s, g));
   return lobe_crop_from_masks(s, grid, s->masks, crop, eligible);
 }
 
@@ -2013,7 +2129,8 @@ lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lo
                                    float* h_out, uint32_t* history, float* cut_history, lobe_block_load* best) {
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
-  if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: use lobe_bo_run with the exchange objective");
+  if (s->world != 1 && !s->comm)
+    return fail(LOBE_E_STATE, "bare shard (world > 1, no communicator): use lobe_bo_run with an exchange objective");
   if (m < 1 || n < 1 || m * n > kMaxBlocks) return fail(LOBE_E_INVALID_CONFIG, "grid m, n");
   lobe_balance_opts o{100, 0, 0.1f, 0.15, 8};
   if (opts) o = *opts;
@@ -2027,13 +2144,14 @@ lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lo
     lobe_grid gr{m, n, v, h, dv, dh, tau};
     GridV g;
     lobe_status st = check_grid(&gr, &g);
-    if (st == LOBE_OK) st = ensure_eval(s, g);
+    if (st == LOBE_OK) st = s->comm ? ensure_xchg(s, g) : ensure_eval(s, g);
     if (st != LOBE_OK) {
       last = st;
       return 1;
     }
+    const uint32_t* gv = s->comm ? s->x_gvis : s->h_gvis();
     uint32_t b = 0;
-    for (int k = 0; k < g.B; ++k) b = std::max(b, s->h_gvis()[k]);
+    for (int k = 0; k < g.B; ++k) b = std::max(b, gv[k]);
     *val = b;
     return 0;
   };

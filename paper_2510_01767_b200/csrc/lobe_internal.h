@@ -101,7 +101,13 @@ struct VisArgs {
   int64_t n_sub;         // ceil(n_cams / 32)
   const float4* slo;     // [n_tiles x 4] slice boxes (256 Gaussians) for k_vis_tiles
   const float4* shi;
-  unsigned long long* counters;  // k_vis_tiles: [0] undecided, [1] accepted (slice, camera) pairs; may be NULL
+  unsigned long long* counters;  // [32]: k_vis_tiles: [0] undecided, [1] accepted (slice, camera) pairs; I16
+                                 // (measured, weighted by the slice's real Gaussians): [9] slice-rejected, [10]
+                                 // slice-accepted, [11] exact-tested tests, [12] / [13] visible bits written for
+                                 // accepted / exact-tested slices ([8]: k_cull's tile-rejected tests);
+                                 // [16 + p]: exact-tested (slice, camera) pairs by open-condition pattern p
+                                 // (isotropic; 9 patterns, see k_vis_tiles); may be NULL
+  int64_t G;                     // real Gaussians (the rest of G_pad is padding)
   int aniso;                     // 1: anisotropic predicate (ledger L24)
   const float4* cv;              // anisotropic: pair-interleaved Sigma
   const AnisoCam* acams;         // anisotropic: per local camera
@@ -116,9 +122,11 @@ struct VisArgs {
 cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_tiles, float4* tlo, float4* thi,
                                float4* slo, float4* shi, cudaStream_t st);
 // hierarchical: chunk boxes (clo/chi scratch, n_tiles/16 each) then tile boxes
-cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float4* chi, int64_t n_tiles,
+// rej_tests (may be NULL): += the real Gaussians of every (tile, camera) pair the
+// chunk or tile bound rejects (I16, measured in the kernel)
+cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float4* chi, int64_t n_tiles, int64_t G,
                         const CamSetup* cams, const AnisoCam* acams, int64_t n_cams, uint32_t* keep, unsigned long long* kept_pairs,
-                        cudaStream_t st);
+                        unsigned long long* rej_tests, cudaStream_t st);
 // kept-camera lists per tile: phase 0 counts, phase 1 fills (after a scan of the counts)
 // per kept (tile, camera) pair (klist order): byte q = box_class of slice q
 // (0 reject, 2 accept, 1 | need << 2 undecided), so the test kernel loads
@@ -193,6 +201,9 @@ cudaError_t launch_block_masks(int64_t n_tiles, const uint32_t* tile_off, const 
                                uint32_t* gvis, cudaStream_t st);
 cudaError_t launch_masks_combine(const uint32_t* gathered, int W, int B, int64_t words, uint32_t* out,
                                  uint32_t* gvis, cudaStream_t st);
+// exchange buffer of the local block counts: out[b] = ncams[b] (u64), out[B + b] = incid[b]
+cudaError_t launch_xcounts(const uint32_t* ncams, const unsigned long long* incid, int B, unsigned long long* out,
+                           cudaStream_t st);
 // a9: caller-order crop / eligible masks.
 // mt: scratch, B x words u32 (word-major transpose of masks)
 // a9: per-Gaussian block bits (scratch mbits, cb8: words * 32 entries each), then the caller-order gather

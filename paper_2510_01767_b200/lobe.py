@@ -25,7 +25,8 @@ EXPORTS = ["lobe_load_scene", "lobe_free_scene", "lobe_last_error", "lobe_assign
            "lobe_masks_combine", "lobe_block_records", "lobe_crop_from_masks", "lobe_export_rows",
            "lobe_get_stats", "lobe_scene_info", "lobe_version", "lobe_dev_vis_bench", "lobe_block_subscene",
            "lobe_densify_step", "lobe_prune_outside", "lobe_merge_blocks", "lobe_render_select",
-           "lobe_camera_clouds", "lobe_render_maps"]
+           "lobe_camera_clouds", "lobe_render_maps", "lobe_nccl_unique_id", "lobe_release_comms",
+           "lobe_xchg_block_loads_host", "lobe_xchg_all_masks_host", "lobe_xchg_gather_cameras_host"]
 
 
 PREDICATE_ISOTROPIC, PREDICATE_ANISOTROPIC = 0, 1  # lobe_options.predicate (DESIGN.md ledger L24)
@@ -82,9 +83,23 @@ class Frame(ctypes.Structure):
                 ("axis_v", ctypes.c_float * 3), ("auto_flags", ctypes.c_uint32)]
 
 
+# lobe_host_comm callbacks (include/lobe.h): 0 = success
+HC_ALL_GATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+HC_ALL_REDUCE_U64 = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t)
+HC_ALL_TO_ALL_V = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t),
+                                   ctypes.POINTER(ctypes.c_size_t), ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t),
+                                   ctypes.POINTER(ctypes.c_size_t))
+
+
+class HostComm(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("all_gather", HC_ALL_GATHER), ("all_reduce_u64", HC_ALL_REDUCE_U64),
+                ("all_to_all_v", HC_ALL_TO_ALL_V)]
+
+
 class Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("stream", ctypes.c_void_p), ("assign_mode", ctypes.c_int32), ("predicate", ctypes.c_int32)]
+                ("stream", ctypes.c_void_p), ("assign_mode", ctypes.c_int32), ("predicate", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("host_comm", ctypes.POINTER(HostComm))]
 
 
 class Grid(ctypes.Structure):
@@ -114,7 +129,9 @@ class Stats(ctypes.Structure):
                 ("t_depth_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_uint64),
                 ("cub_launches", ctypes.c_uint64), ("kept_tests", ctypes.c_uint64),
-                ("accepted_tests", ctypes.c_uint64), ("exact_variant_tests", ctypes.c_uint64 * 6)]
+                ("accepted_tests", ctypes.c_uint64), ("exact_variant_tests", ctypes.c_uint64 * 6),
+                ("decided_tests", ctypes.c_uint64 * 4), ("visible_bits", ctypes.c_uint64 * 2),
+                ("exact_pattern_tests", ctypes.c_uint64 * 9)]
 
 
 OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
@@ -162,8 +179,16 @@ def lib():
         L.lobe_export_rows.argtypes = [vp, i64, i64, vp]
         L.lobe_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
         L.lobe_dev_vis_bench.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
+        L.lobe_nccl_unique_id.argtypes = [vp]
+        L.lobe_release_comms.argtypes = []
+        L.lobe_release_comms.restype = None
+        HCP, sz = ctypes.POINTER(HostComm), ctypes.c_size_t
+        L.lobe_xchg_block_loads_host.argtypes = [HCP, i32, i32, i32, sz, vp, vp, vp, vp, vp]
+        L.lobe_xchg_all_masks_host.argtypes = [HCP, i32, i32, i32, sz, vp, vp]
+        L.lobe_xchg_gather_cameras_host.argtypes = [HCP, i32, i32, i64, sz, vp, vp]
         for name in EXPORTS:
-            if name not in ("lobe_last_error", "lobe_version", "lobe_mask_words", "lobe_free_scene"):
+            if name not in ("lobe_last_error", "lobe_version", "lobe_mask_words", "lobe_free_scene",
+                            "lobe_release_comms"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -221,11 +246,13 @@ class Scene:
     """Owning wrapper of a lobe_scene* handle."""
 
     def __init__(self, gaussians, cameras, frame=None, device=0, rank=0, world=1, stream=None,
-                 assign_mode=ASSIGN_RATIO, predicate=0):
+                 assign_mode=ASSIGN_RATIO, predicate=0, nccl_id=None, host_comm=None):
         """gaussians: an object with x..opacity attributes (numpy host arrays or
         torch CUDA tensors); cameras: a synth Scene (its camera arrays) or a
         ctypes Camera array. frame: dict(center, radius, axis_u, axis_v) or None
-        (automatic, ledger L12)."""
+        (automatic, ledger L12). nccl_id (128 bytes from nccl_unique_id(), the
+        same on every rank) or host_comm (a HostComm): the scene's communicator --
+        every call is then collective and returns global outputs (include/lobe.h)."""
         L = lib()
         self._keep = []
         names = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
@@ -256,7 +283,13 @@ class Scene:
             fr.axis_v[:] = [float(v) for v in frame["axis_v"]]
         fr.auto_flags = flags
         st = stream if (stream is None or isinstance(stream, int)) else stream.cuda_stream
-        opt = Options(int(device), int(rank), int(world), st, int(assign_mode), int(predicate))
+        opt = Options(int(device), int(rank), int(world), st, int(assign_mode), int(predicate), None, None)
+        if nccl_id is not None:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opt.nccl_unique_id = ctypes.addressof(self._nccl_id)
+        if host_comm is not None:
+            self._host_comm = host_comm  # the callbacks must outlive the scene
+            opt.host_comm = ctypes.pointer(host_comm)
         h = ctypes.c_void_p()
         _check(L.lobe_load_scene(ctypes.byref(g), cams, len(cams), ctypes.byref(fr), ctypes.byref(opt),
                                  ctypes.byref(h)))
@@ -266,6 +299,8 @@ class Scene:
         info = [ctypes.c_int64() for _ in range(4)]
         _check(L.lobe_scene_info(h, *[ctypes.byref(x) for x in info]))  # does not wait for the device
         self.G, self.N, self.n_local, self.cam_begin = [x.value for x in info]
+        self.collective = nccl_id is not None or host_comm is not None
+        self.n_out = self.N if (self.collective or world == 1) else self.n_local  # per-camera output rows
 
     def close(self):
         if getattr(self, "handle", None):
@@ -292,7 +327,7 @@ class Scene:
 
     def assign_cameras(self, m, n, **grid_kw):
         g, keep = make_grid(m, n, **grid_kw)
-        NL, B = self.n_local, m * n
+        NL, B = self.n_out, m * n
         out = dict(K=np.empty(NL, np.uint32), D=np.empty(NL, np.float64), zmin=np.empty(NL, np.float32),
                    zmax=np.empty(NL, np.float32), n=np.empty((NL, B), np.uint32), n0=np.empty((NL, B), np.uint32),
                    member=np.empty(NL, np.uint64), home=np.empty(NL, np.int32))
@@ -504,3 +539,47 @@ def bo_run(m, n, objective, L=100, seed=0, n_sobol=8):
         raise errs[0]
     _check(code)
     return dict(v=v[:m - 1], h=h[:n - 1], history=hist, cut_history=ch[:, :D])
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId for Scene(nccl_id=...) (rank 0 creates, every rank uses)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().lobe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def release_comms():
+    lib().lobe_release_comms()
+
+
+def xchg_block_loads_host(comm, rank, world, B, words, partial, counts_local):
+    """lobe_xchg_block_loads_host: the library's exchange choreography on host
+    buffers (partial: B x words u32, counts_local: 2B u64) -> own, g_vis, counts."""
+    partial = np.ascontiguousarray(partial, np.uint32)
+    counts_local = np.ascontiguousarray(counts_local, np.uint64)
+    nb = (rank + 1) * B // world - rank * B // world
+    own = np.zeros((max(nb, 1), words), np.uint32)
+    gv = np.zeros(B, np.uint32)
+    cg = np.zeros(2 * B, np.uint64)
+    _check(lib().lobe_xchg_block_loads_host(ctypes.byref(comm), rank, world, B, words, _ptr(partial),
+                                            _ptr(counts_local), _ptr(own), _ptr(gv), _ptr(cg)))
+    return own[:nb], gv, cg
+
+
+def xchg_all_masks_host(comm, rank, world, B, words, own):
+    own = np.ascontiguousarray(own, np.uint32)
+    out = np.zeros((B, words), np.uint32)
+    _check(lib().lobe_xchg_all_masks_host(ctypes.byref(comm), rank, world, B, words,
+                                          _ptr(own) if own.size else None, _ptr(out)))
+    return out
+
+
+def xchg_gather_cameras_host(comm, rank, world, N, local):
+    """local: this rank's shard rows (numpy, any dtype / trailing shape) -> all N."""
+    local = np.ascontiguousarray(local)
+    elem = local.itemsize * int(np.prod(local.shape[1:], dtype=np.int64))
+    out = np.zeros((N,) + local.shape[1:], local.dtype)
+    _check(lib().lobe_xchg_gather_cameras_host(ctypes.byref(comm), rank, world, N, elem,
+                                               _ptr(local) if local.size else None, _ptr(out)))
+    return out
+

@@ -52,6 +52,18 @@ def _cmp_loads(L, o):
     assert L["objective"] == o["objective"]
 
 
+def check_i16(st, G, n_local, K_sum):
+    """I16, measured inside the kernels: every one of the G x N_local
+    logical tests of the visibility pass was decided exactly once -- by k_cull's
+    chunk / tile bound, by k_vis_tiles' slice bound (rejected / accepted) or by
+    the exact test -- and the visible bits the kernel wrote add up to sum_c K_c
+    (K comes from the separate depth-statistic kernel)."""
+    d = [int(x) for x in st.decided_tests]
+    assert sum(d) == G * n_local, (d, G, n_local)
+    assert int(st.visible_bits[0]) + int(st.visible_bits[1]) == int(K_sum)
+    assert d[3] <= st.dense_tests and d[2] <= st.accepted_tests  # padding only adds to the executed counts
+
+
 def full_parity(sc, grids, mode=0, predicate=0):
     lobe = _lobe()
     with lobe.Scene(sc, sc, assign_mode=mode, predicate=predicate) as S:
@@ -61,6 +73,8 @@ def full_parity(sc, grids, mode=0, predicate=0):
         rows = S.export_rows()
         assert (rows == o0["vis"]["rows"]).all()
         st = S.stats()
+        check_i16(st, sc.G, sc.N, np.asarray(o0["vis"]["K"], np.int64).sum())
+        assert st.tests_executed == sc.G * sc.N
         for g in grids:
             o = o0 if g is grids[0] else None
             if o is None:
@@ -272,7 +286,8 @@ def test_world_shards_match_world1():
 def test_bo_trajectory_parity_and_I16():
     """Every evaluation of lobe_balance_partition equals the oracle objective at
     the recorded cuts (so the oracle-backed run follows the same trajectory), and
-    the visibility kernel ran exactly once: tests_executed = G N (I16)."""
+    the visibility kernels ran exactly once: tests_executed, the sum of the
+    kernels' own decision counters, = G N (I16)."""
     lobe = _lobe()
     sc = make_scene(make_config("building", G=40_000, N=48, seed=0x42))
     m, n = sc.cfg.m, sc.cfg.n
@@ -285,6 +300,7 @@ def test_bo_trajectory_parity_and_I16():
         assert r["best"]["objective"] == r["history"].min() <= r["history"][0]
         st = S.stats()
         assert st.tests_executed == sc.G * sc.N and st.vis_launches == 1
+        check_i16(st, sc.G, sc.N, np.asarray(o["vis"]["K"], np.int64).sum())
 
 
 @pytest.mark.parametrize("name", ["rubble", "building", "residence", "matrixcity"])
@@ -309,6 +325,7 @@ def test_full_size_sampled(name):
         asg = oracle.assign(sc, pre, vis, g)
         a = S.assign_cameras(m, n)
         _cmp_percam(a, vis, asg, sel=sel)
+        check_i16(S.stats(), sc.G, sc.N, a["K"].astype(np.int64).sum())
         L = S.block_loads(m, n)
         assert int(L["incidences"].sum()) == int(a["K"].astype(np.int64).sum())      # I2
         assert int(L["g_blk"].astype(np.int64).sum()) == sc.G                         # I4
