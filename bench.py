@@ -533,11 +533,12 @@ def main():
         dense_ref["frac"] = dense_ref["achieved"] / peak
         dense_ref["basis"] = "22 flop x G x N_local (every test executed) / the kernel's CUDA-event time"
         roof["dense_reference"] = dense_ref
-    tj = load_profile("ncu_visibility_traffic.json", cfg_name, world, pred)
-    if tj:
-        roof["traffic"] = tj.get("dram_bytes_per_launch")
     nc = load_profile("r02_vis_tiles_ncu.json", cfg_name, world, pred)
     if nc:
+        # DRAM bytes of one k_vis_tiles launch (the pass's dominant kernel) from the committed
+        # ncu --set full capture; algorithmic: 16 B x G_pad read + the kept pairs' row words
+        roof["traffic"] = nc.get("dram_bytes_per_launch")
+        roof["traffic_kernel"] = "k_vis_tiles (profiles/r02_vis_tiles_ncu.json)"
         roof["ncu"] = {k: nc[k] for k in nc if k not in ("config", "world")}
     # the depth statistic (a4): 9 flop per visible (Gaussian, camera) incidence
     # (w: 3 FMA, o*w: 1 FMA, o: 1 add), the statistic's own work

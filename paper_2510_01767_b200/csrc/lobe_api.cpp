@@ -28,6 +28,8 @@
 #include "lobe_internal.h"
 #include "lobe_comm.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace lobe;
 
 namespace lobe {
@@ -60,6 +62,14 @@ lobe_status fail(lobe_status st, const std::string& msg) {
   g_err = msg;
   return st;
 }
+
+// NVTX range per exported call (nsys / ncu --nvtx show the API structure; a
+// no-op unless a tool injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define LOBE_NVTX(name) NvtxRange nvtx_range_(name)
 
 #define CK(call)                                                                                   \
   do {                                                                                             \
@@ -128,6 +138,11 @@ struct lobe_scene {
   uint8_t* flags = nullptr;     // dev bench (camera-inner variants) only
   uint8_t* nonempty = nullptr;  // [kept pairs] any Gaussian visible
   PairPartial* pair_part = nullptr;
+  // a4 deferred until needed (ensure_a4)
+  bool a4_pending = false;
+  uint32_t* camtile = nullptr;  // camera x tile bits of the non-empty pairs (a4's camera order)
+  int64_t a4_cap = 0, a4_tw = 0;
+  unsigned long long a4_kept = 0;
   uint32_t* cam_off = nullptr;
   int32_t* cam_order = nullptr;
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
@@ -516,7 +531,6 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
     a.dz = s->dz;
     a.hist = s->hist;
     a.nzp = nzp;
-    a.K = s->cloud_mode ? s->cloud_K : s->K;
     a.cam_gu = s->d_cam_gu;
     a.cam_gv = s->d_cam_gv;
     a.n_cams = s->N_loc;
@@ -920,9 +934,47 @@ lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<ui
   return LOBE_OK;
 }
 
+
+// a4, the per-camera depth statistic over the non-empty (tile, camera) pairs of
+// the load pass, enqueued on the scene's stream once (see lobe_load_scene).
+lobe_status ensure_a4(lobe_scene* s) {
+  if (!s->a4_pending) return LOBE_OK;
+  s->a4_pending = false;
+  cudaStream_t st = s->stream;
+  const int64_t NL = std::max<int64_t>(s->N_loc, 1), cap = s->a4_cap, tw = s->a4_tw;
+  CK(cudaEventRecord(s->ev[11], st));
+  if (s->N_loc > 0) {
+    KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words,
+                          reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk),
+                          reinterpret_cast<const float2*>(s->o2), s->cams, s->pair_part, st));
+    // pair indices in camera-major order, tile order within a camera
+    uint32_t *ccount = nullptr, *wordpre = nullptr;
+    CK(s->alloc(&ccount, (size_t)NL + 1));
+    CK(s->alloc(&wordpre, (size_t)NL * tw));
+    CK(cudaMemsetAsync(ccount + NL, 0, sizeof(uint32_t), st));
+    KL(launch_cam_order(s->N_loc, tw, s->camtile, wordpre, ccount, st));
+    size_t sb2 = 0;
+    CK(exclusive_scan_u32(nullptr, sb2, ccount, s->cam_off, NL + 1, st));
+    void* tmp2 = nullptr;
+    CK(malloc_async(&tmp2, sb2, st));
+    CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
+    cudaFreeAsync(tmp2, st);
+    s->release(ccount);
+    if (s->a4_kept > 0)
+      KL(launch_cam_scatter(s->tile_off, s->n_tiles, cap, s->pair_cam, s->pair_tile, s->camtile, wordpre, tw,
+                            s->cam_off, s->cam_order, st));
+    s->release(wordpre);
+    KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
+  }
+  s->release(s->camtile);
+  CK(cudaEventRecord(s->ev[12], st));
+  return LOBE_OK;
+}
+
 // Load-pass timings and counters (events and pinned counters of the last load).
 void finalize_load_stats(lobe_scene* s) {
   if (!s->stats_pending) return;
+  ensure_a4(s);
   cudaStreamSynchronize(s->stream);
   s->st.t_prep_ms = ms_between(s->ev[0], s->ev[1]);
   // visibility pass = culling kernel + test kernel (list building excluded)
@@ -1084,6 +1136,7 @@ lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used
     }
   }
   CK(cudaStreamWaitEvent(s->side, after ? after : s->ev[4], 0));
+  CK(cudaStreamWaitEvent(s->side, s->ev[12], 0));  // a4 (K, D, z_min, z_max), launched before the copies
   for (size_t i = 0; i < plan.size(); ++i)
     CK(cudaMemcpyAsync(s->pin_out + plan[i].off, srcs[i], plan[i].bytes, cudaMemcpyDeviceToHost, s->side));
   CK(cudaStreamSynchronize(s->side));
@@ -1123,7 +1176,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
   s->release(s->ncb); s->release(s->n0cb); s->release(s->member); s->release(s->sel); s->release(s->home);
-  s->release(s->counts); s->incid = nullptr; s->release(s->masks);
+  s->release(s->counts); s->incid = nullptr; s->release(s->masks); s->release(s->camtile);
   s->release(s->own_masks); s->release(s->d_xcounts);
   cudaStreamSynchronize(s->stream);
   delete s->xops;
@@ -1140,6 +1193,7 @@ void lobe_free_scene(lobe_scene* s) {
 
 lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, int64_t n_cams, lobe_frame* inout_frame,
                             const lobe_options* opt, lobe_scene** out) {
+  LOBE_NVTX("lobe_load_scene");
   g_err.clear();
   if (!out) return fail(LOBE_E_INVALID_CONFIG, "out is NULL");
   *out = nullptr;
@@ -1460,42 +1514,23 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     const int64_t tw = (s->n_tiles + 31) / 32;
     CK(s->alloc(&s->pair_cam, (size_t)cap));
     CK(s->alloc(&s->pair_tile, (size_t)cap));
-    uint32_t *camtile = nullptr, *wordpre = nullptr;
+    uint32_t* camtile = nullptr;
     CK(s->alloc(&camtile, (size_t)NL * tw));
     CK(cudaMemsetAsync(camtile, 0, sizeof(uint32_t) * NL * tw, st));
     if (s->N_loc > 0 && kept_pairs > 0)
       KL(launch_tile_fill(s->koff, s->klist, s->nonempty, s->n_tiles, s->tile_off, s->pair_cam, s->pair_tile,
                           camtile, tw, st));
-    // ---- a4 depth statistic over the non-empty (tile, camera) pairs
-    CK(cudaEventRecord(s->ev[11], st));
+    // ---- a4 depth statistic: deferred (ensure_a4) -- enqueued by the first call
+    // that needs it, or right after the first crop kernel, whose device->host copy
+    // then overlaps it; the assignment does not need it (K_c = sum_b n0_cb, I5)
+    s->camtile = camtile;
+    s->a4_cap = cap;
+    s->a4_tw = tw;
+    s->a4_kept = kept_pairs;
+    s->a4_pending = true;
     CK(s->alloc(&s->pair_part, (size_t)cap));
     CK(s->alloc(&s->cam_off, (size_t)NL + 1));
     CK(s->alloc(&s->cam_order, (size_t)cap));
-    if (s->N_loc > 0) {
-      KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words, reinterpret_cast<const float4*>(s->xy),
-                            reinterpret_cast<const float4*>(s->zk), reinterpret_cast<const float2*>(s->o2), s->cams,
-                            s->pair_part, st));
-      // pair indices in camera-major order, tile order within a camera
-      uint32_t* ccount;
-      CK(s->alloc(&ccount, (size_t)NL + 1));
-      CK(s->alloc(&wordpre, (size_t)NL * tw));
-      CK(cudaMemsetAsync(ccount + NL, 0, sizeof(uint32_t), st));
-      KL(launch_cam_order(s->N_loc, tw, camtile, wordpre, ccount, st));
-      size_t sb2 = 0;
-      CK(exclusive_scan_u32(nullptr, sb2, ccount, s->cam_off, NL + 1, st));
-      void* tmp2 = nullptr;
-      CK(malloc_async(&tmp2, sb2, st));
-      CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
-      cudaFreeAsync(tmp2, st);
-      s->release(ccount);
-      if (kept_pairs > 0)
-        KL(launch_cam_scatter(s->tile_off, s->n_tiles, cap, s->pair_cam, s->pair_tile, camtile, wordpre, tw,
-                              s->cam_off, s->cam_order, st));
-      s->release(wordpre);
-      KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
-    }
-    s->release(camtile);
-    CK(cudaEventRecord(s->ev[12], st));
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
     CK(s->alloc(&s->word_zone, (size_t)s->words));
@@ -1538,12 +1573,14 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
 
 lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* K, double* depth_mean, float* z_min,
                                 float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member, int32_t* home) {
+  LOBE_NVTX("lobe_assign_cameras");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   CK(cudaSetDevice(s->device));
   GridV g;
   TRY(check_grid(grid, &g));
   TRY(ensure_eval(s, g));
+  TRY(ensure_a4(s));  // K, D, z_min, z_max
   const size_t NL = (size_t)s->N_loc;
   std::vector<StagedCopy> plan;
   std::vector<const void*> srcs;
@@ -1592,6 +1629,7 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
 }
 
 lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
+  LOBE_NVTX("lobe_block_loads");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (s->world != 1 && !s->comm)
@@ -1614,6 +1652,7 @@ lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_lo
 }
 
 lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
+  LOBE_NVTX("lobe_crop_masks");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (s->world != 1 && !s->comm)
@@ -1630,6 +1669,7 @@ lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop
 
 lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
                                  uint64_t* eligible) {
+  LOBE_NVTX("lobe_crop_from_masks");
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   CK(cudaSetDevice(s->device));
   GridV g;
@@ -1672,27 +1712,30 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   CK(cudaEventRecord(s->ev[14], s->stream));
   KLN(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream), 2);
   CK(cudaEventRecord(s->ev[15], s->stream));
-  if (crop && !crop_dev) {
-    TRY(copy_out(s, crop, dc, bytes));
-    s->release(dc);
+  // a pending a4 (depth statistic) goes on the scene's stream now, so it runs
+  // while the masks travel to the host on the side stream (copy engines)
+  TRY(ensure_a4(s));
+  const bool host_out = (crop && !crop_dev) || (eligible && !elig_dev);
+  if (host_out) {
+    if (!s->side) s->side = acquire_side_stream(s->device);
+    if (!s->side) return fail(LOBE_E_CUDA, "side stream creation failed");
+    CK(cudaStreamWaitEvent(s->side, s->ev[15], 0));
+    if (crop && !crop_dev) CK(cudaMemcpyAsync(crop, dc, bytes, cudaMemcpyDefault, s->side));
+    if (eligible && !elig_dev) CK(cudaMemcpyAsync(eligible, de, bytes, cudaMemcpyDefault, s->side));
+    CK(cudaStreamSynchronize(s->side));  // host outputs are complete on return
+    s->st.t_crop_ms = ms_between(s->ev[14], s->ev[15]);
   }
-  if (eligible && !elig_dev) {
-    TRY(copy_out(s, eligible, de, bytes));
-    s->release(de);
-  }
+  if (crop && !crop_dev) s->release(dc);    // the copies are done: stream-ordered frees are safe
+  if (eligible && !elig_dev) s->release(de);
   s->release(mbits);
   s->release(cb8);
-  if ((crop && !crop_dev) || (eligible && !elig_dev)) {
-    CK(cudaStreamSynchronize(s->stream));  // host outputs are complete on return
-    s->st.t_crop_ms = ms_between(s->ev[14], s->ev[15]);
-  } else {
-    s->crop_pending = true;  // device outputs: stream-ordered; timing read lazily
-  }
+  if (!host_out) s->crop_pending = true;  // device outputs: stream-ordered; timing read lazily
   return LOBE_OK;
 }
 
 lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
                                uint64_t* incid) {
+  LOBE_NVTX("lobe_block_partial");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (!d_masks) return fail(LOBE_E_INVALID_CONFIG, "d_masks NULL");
@@ -1709,6 +1752,7 @@ lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d
 
 lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
                                uint32_t* g_vis) {
+  LOBE_NVTX("lobe_masks_combine");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (B < 1 || B > kMaxBlocks || W < 1) return fail(LOBE_E_INVALID_CONFIG, "bad B or W");
@@ -1725,6 +1769,7 @@ lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathe
 
 lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint32_t* n_cams, const uint64_t* incid,
                                const uint32_t* g_vis, lobe_block_load* out, uint32_t* objective) {
+  LOBE_NVTX("lobe_block_records");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   GridV g;
@@ -1735,6 +1780,7 @@ lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint3
 }
 
 lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t* rows) {
+  LOBE_NVTX("lobe_export_rows");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (c0 < 0 || count < 0 || c0 + count > s->N_loc) return fail(LOBE_E_INVALID_INDEX, "camera range");
@@ -1751,6 +1797,7 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
 }
 
 lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
+  LOBE_NVTX("lobe_dev_vis_bench");
   // variant 0: tile-major kernel over the kept lists (production);
   // 1-5: the camera-inner kernel (1 = culled, 2 = dense: every test evaluated)
   g_err.clear();
@@ -1798,6 +1845,7 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
 
 lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
                                 lobe_subscene* out, int64_t capacity) {
+  LOBE_NVTX("lobe_block_subscene");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (s->world != 1) return fail(LOBE_E_STATE, "world > 1: not supported for the block pipeline");
@@ -1855,6 +1903,7 @@ lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t bl
 lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
                               const float* grad, const float* normals, float tau_grad, float scale_split,
                               lobe_subscene* out, int64_t capacity) {
+  LOBE_NVTX("lobe_densify_step");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   TRY(check_sub(in, in && in->n > 0, "in"));
@@ -1888,6 +1937,7 @@ lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t bloc
 
 lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
                                lobe_subscene* out, int64_t capacity) {
+  LOBE_NVTX("lobe_prune_outside");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   TRY(check_sub(in, in && in->n > 0, "in"));
@@ -1918,6 +1968,7 @@ lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t blo
 
 lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
                               int64_t capacity) {
+  LOBE_NVTX("lobe_merge_blocks");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (count < 0 || (count > 0 && !subs)) return fail(LOBE_E_INVALID_CONFIG, "subs");
@@ -2022,6 +2073,7 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
 
 lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
                                float eps_w) {
+  LOBE_NVTX("lobe_render_select");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   CK(cudaSetDevice(s->device));
@@ -2050,6 +2102,7 @@ lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int3
 }
 
 lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity) {
+  LOBE_NVTX("lobe_camera_clouds");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (!s->cloud_mode) return fail(LOBE_E_STATE, "no clouds: call lobe_render_select first");
@@ -2071,6 +2124,7 @@ lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float
 
 lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
                              float* depth, float* weight) {
+  LOBE_NVTX("lobe_render_maps");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (camera < 0 || camera >= s->N_loc) return fail(LOBE_E_INVALID_INDEX, "camera");
@@ -2087,6 +2141,7 @@ lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_
 
 lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* n_cameras, int64_t* n_local_cameras,
                             int64_t* cam_begin) {
+  LOBE_NVTX("lobe_scene_info");
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (n_gaussians) *n_gaussians = s->st.n_gaussians;
   if (n_cameras) *n_cameras = s->st.n_cameras;
@@ -2096,6 +2151,7 @@ lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* 
 }
 
 lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
+  LOBE_NVTX("lobe_get_stats");
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
   finalize_load_stats(const_cast<lobe_scene*>(s));
   const_cast<lobe_scene*>(s)->wait_counts();
@@ -2111,6 +2167,7 @@ lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
 
 lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lobe_objective_fn objective, void* ctx,
                         float* v_out, float* h_out, uint32_t* history, float* cut_history) {
+  LOBE_NVTX("lobe_bo_run");
   g_err.clear();
   if (m < 1 || n < 1 || m * n > kMaxBlocks) return fail(LOBE_E_INVALID_CONFIG, "grid m, n");
   if (!objective) return fail(LOBE_E_INVALID_CONFIG, "objective NULL");
@@ -2127,6 +2184,7 @@ lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lob
 
 lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lobe_balance_opts* opts, float* v_out,
                                    float* h_out, uint32_t* history, float* cut_history, lobe_block_load* best) {
+  LOBE_NVTX("lobe_balance_partition");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
   if (s->world != 1 && !s->comm)

@@ -180,7 +180,6 @@ struct AssignArgs {
   const ZoneTables* dz;
   const uint32_t* hist;
   int nzp;
-  const uint32_t* K;
   const float* cam_gu;
   const float* cam_gv;
   int64_t n_cams;

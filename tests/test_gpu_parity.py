@@ -551,6 +551,26 @@ def test_aniso_edge_clusters_exact(seed):
     assert st.dense_tests > 0
 
 
+def test_aniso_overflowing_covariance_not_accepted():
+    """scales up to 1e18 are valid (L22); a tight cluster of such
+    Gaussians projecting inside the image has A = C = inf in the pinned fp32
+    covariance, d = A - C = NaN and the oracle calls it invisible. The slice
+    bound must then leave the slice to the exact test instead of accepting it."""
+    rng = np.random.default_rng(7)
+    g = [dict(mu=[float(x), float(y), 1.0 + float(z)], s=1e18, o=0.9)
+         for x, y, z in rng.normal(scale=0.002, size=(300, 3))]
+    g += [dict(mu=[float(x), float(y), float(z)], s=0.001, o=0.8)
+          for x, y, z in zip(rng.uniform(-0.5, 0.5, 200), rng.uniform(-0.5, 0.5, 200), rng.uniform(0.5, 3, 200))]
+    cam1 = dict(GOLD["camera_C0"])
+    cam2 = dict(GOLD["camera_C0"], t=[-0.3, 0.1, 0.0])
+    sc = mini_scene(g, [cam1, cam2])
+    o = oracle.run(sc, predicate=1)
+    huge = np.unpackbits(o["vis"]["rows"].view(np.uint8), axis=1, bitorder="little")[:, :300]
+    assert not huge.any()  # NaN footprint: never visible in O6a
+    assert o["vis"]["K"].min() > 0
+    full_parity(sc, [oracle.default_grid(1, 1), oracle.default_grid(2, 2)], predicate=1)
+
+
 @pytest.mark.parametrize("name", ["rubble", "matrixcity"])
 def test_full_size_sampled_aniso(name):
     """The anisotropic mode at full Rubble and MatrixCity size: rows and
