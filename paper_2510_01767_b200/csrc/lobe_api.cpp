@@ -71,6 +71,20 @@ struct NvtxRange {
 };
 #define LOBE_NVTX(name) NvtxRange nvtx_range_(name)
 
+// LOBE_TRACE_HOST=1: host timeline of lobe_load_scene (diagnosis of GPU idle gaps)
+struct HostTimeline {
+  const bool on = std::getenv("LOBE_TRACE_HOST") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lobe host] %-28s +%8.1f us  (%8.1f us)\n", what,
+                 std::chrono::duration<double, std::micro>(t - last).count(),
+                 std::chrono::duration<double, std::micro>(t - t0).count());
+    last = t;
+  }
+};
+
 #define CK(call)                                                                                   \
   do {                                                                                             \
     cudaError_t e_ = (call);                                                                       \
@@ -1194,6 +1208,7 @@ void lobe_free_scene(lobe_scene* s) {
 lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, int64_t n_cams, lobe_frame* inout_frame,
                             const lobe_options* opt, lobe_scene** out) {
   LOBE_NVTX("lobe_load_scene");
+  HostTimeline tl;
   g_err.clear();
   if (!out) return fail(LOBE_E_INVALID_CONFIG, "out is NULL");
   *out = nullptr;
@@ -1215,6 +1230,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   if (inout_frame) F = *inout_frame;
   else F.auto_flags = LOBE_FRAME_AUTO_ALL;
   TRY(resolve_frame(cams, n_cams, &F));
+  tl.mark("resolve_frame");
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LOBE_E_CUDA, "no CUDA device");
@@ -1241,6 +1257,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     delete s;
     return fail(LOBE_E_CUDA, "pinned staging allocation failed");
   }
+  tl.mark("scene setup");
   lobe_status rs = [&]() -> lobe_status {
     cudaStream_t st = s->stream;
     {  // communicator first: NCCL creation is collective (every rank is in this call)
@@ -1263,6 +1280,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     const int64_t cam_end = (int64_t)(o.rank + 1) * n_cams / o.world;
     s->N_loc = cam_end - s->cam_begin;
 
+    tl.mark("comm");
     CK(cudaEventRecord(s->ev[0], st));
     // ---- inputs on device
     const float* src[11] = {g->x, g->y, g->z, g->sx, g->sy, g->sz, g->qw, g->qx, g->qy, g->qz, g->opacity};
@@ -1306,7 +1324,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     pin.rho = F.radius;
     pin.cov = cov_raw;
+    tl.mark("inputs + a1 allocs");
     KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
+    tl.mark("k_prep_raw launched");
     // validation flags and the ground min / max reach the host asynchronously;
     // they are checked at the first synchronisation (after the culling pass)
     CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
@@ -1324,6 +1344,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->iperm, (size_t)G));
     if (s->aniso) CK(s->alloc(&s->cv, (size_t)s->G_pad / 2 * 3));
     KL(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st));
+    tl.mark("sort + k_pack launched");
     s->release(cov_raw);
     cudaFreeAsync(tmp, st);
     s->release(rec);
@@ -1381,6 +1402,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // ---- a3/a4 visibility pass
     CK(s->alloc(&s->rows, (size_t)NL * s->words));
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
+    tl.mark("camera setup + bounds");
     CK(cudaEventRecord(s->ev[1], st));
     CK(cudaMemsetAsync(s->kept, 0, sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(s->vcnt, 0, 32 * sizeof(unsigned long long), st));
@@ -1421,8 +1443,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       cudaFreeAsync(tu, st);
     }
     CK(cudaMemcpyAsync(&s->pin->n_units, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    tl.mark("cull + lists launched");
     TRY(validate_cameras(cams, n_cams));  // host work overlapping the device's a1 / culling
+    tl.mark("validate_cameras");
     CK(cudaStreamSynchronize(st));
+    tl.mark("sync (kept pairs)");
     const unsigned long long kept_pairs = s->pin->kept_pairs;
     const uint32_t nu = s->pin->n_units;
     s->n_units = nu;
@@ -1547,6 +1572,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       s->incid = reinterpret_cast<unsigned long long*>(s->counts + 3 * kMaxBlocks);
     }
     CK(cudaEventRecord(s->ev[3], st));
+    tl.mark("rest enqueued");
     // no synchronisation here: the depth statistic may still run while the caller
     // enqueues the next call; event timings are read lazily (finalize_load_stats)
     s->kept_pairs_last = kept_pairs;
