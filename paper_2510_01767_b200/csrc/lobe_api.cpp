@@ -132,7 +132,7 @@ struct DevBuf {
 
 }  // namespace
 
-constexpr int kNumEvents = 20;
+constexpr int kNumEvents = 23;
 
 struct lobe_scene {
   int device = 0;
@@ -222,6 +222,8 @@ struct lobe_scene {
     uint32_t n_units;                       // visibility work units of the last load
     unsigned long long kept_pairs;          // (tile, camera) pairs kept by the culling pass
     unsigned long long prep_bad;            // k_prep_raw: first invalid Gaussian
+    uint32_t q_err;                         // k_check_quats (deferred path): any invalid quaternion
+    unsigned long long q_bad;               // k_check_quats: first invalid quaternion
   };
   static_assert(offsetof(Pinned, incid) == offsetof(Pinned, counts) + 3 * kMaxBlocks * sizeof(uint32_t),
                 "pinned counts / incid must mirror the contiguous device block");
@@ -249,7 +251,9 @@ struct lobe_scene {
   // stats
   lobe_stats st{};
   cudaEvent_t ev[kNumEvents] = {};  // load pass: 0, 1, 8-12, 16, 17; evaluation: 2-4, 13; combine: 5, 6; dev bench:
-                                    // 6, 7; crop: 14, 15; collective exchange: 18, 19
+                                    // 6, 7; crop: 14, 15; collective exchange: 18, 19; deferred quaternion
+                                    // check: 20 (done), 21 (k_prep_raw done), 22 (camera copies done)
+  cudaStream_t qstream = nullptr;   // host inputs, isotropic: quaternion copy + check (side stream)
   // ---- communicator: collective calls, global outputs
   lobe::Comm* comm = nullptr;
   lobe::XOps* xops = nullptr;       // device-memory ops of comm on `stream`
@@ -469,6 +473,17 @@ void build_axis(int count, const std::vector<float>& cuts, float delta, AxisZone
       if (in_interval(rep, lo[p], hi[p])) A->cell[z] = (uint8_t)p;
       if (in_interval(rep, elo[p], ehi[p])) A->encl[z] |= 1ull << p;
     }
+  }
+  // zone of x = #{k in [1, K-1] : P[k] <= x} (x < 1); per bin, that count at the
+  // bin's lower end (exact: b / 1024 is a float) and how many breakpoints lie
+  // strictly inside the bin
+  int zlo = 0;  // #{k >= 1 : P[k] <= x0}, nondecreasing in b (P ascending)
+  for (int b = 0; b < kZoneBins; ++b) {
+    const float x0 = (float)b / (float)kZoneBins, x1 = (float)(b + 1) / (float)kZoneBins;
+    while (zlo + 1 < K && P[zlo + 1] <= x0) ++zlo;
+    int nin = 0;
+    for (int k = zlo + 1; k < K && P[k] < x1 && nin < 2; ++k) ++nin;
+    A->bin[b] = (uint16_t)(zlo | ((nin == 0 ? 0 : (nin == 1 ? 1 : 2)) << 14));
   }
 }
 
@@ -994,7 +1009,7 @@ void finalize_load_stats(lobe_scene* s) {
   // visibility pass = culling kernel + test kernel (list building excluded)
   s->st.t_cull_ms = ms_between(s->ev[1], s->ev[8]);
   // slice classification (k_slice_codes) is part of the test decision
-  const float t_codes = (!s->aniso && s->kept_pairs_last > 0) ? ms_between(s->ev[16], s->ev[17]) : 0.f;
+  const float t_codes = (s->kept_pairs_last > 0) ? ms_between(s->ev[16], s->ev[17]) : 0.f;
   s->st.t_vis_ms = s->st.t_cull_ms + t_codes + ms_between(s->ev[9], s->ev[10]);
   s->st.t_depth_ms = ms_between(s->ev[11], s->ev[12]);
   s->n_pairs = s->pin->n_pairs;
@@ -1199,6 +1214,10 @@ void lobe_free_scene(lobe_scene* s) {
     cudaStreamSynchronize(s->side);
     recycle_side_stream(s->device, s->side);  // stream creation costs ~0.4 ms: reuse across scenes
   }
+  if (s->qstream) {
+    cudaStreamSynchronize(s->qstream);
+    recycle_side_stream(s->device, s->qstream);
+  }
   recycle_events(s->device, s->ev);  // event creation costs ~2 us each: reuse across scenes
   recycle_pinned(s->pin);
   recycle_pinned_out(s->pin_out, s->pin_out_cap);
@@ -1288,15 +1307,37 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       if (!src[k]) return fail(LOBE_E_INVALID_CONFIG, "gaussian array NULL");
     float* dev_in = nullptr;
     const float* din[11];
+    // host inputs in the isotropic mode: the quaternions are only validated, so
+    // they travel last on a side stream (with their check) while the device runs
+    // a1 / a3 on the other fields; the verdict is read before the load returns
+    const bool q_defer = !g->on_device && !s->aniso;
+    uint32_t* q_flags = nullptr;  // [0] err, [1..2] first bad index (u64)
     if (!g->on_device) {
       CK(s->alloc(&dev_in, (size_t)11 * G));
       for (int k = 0; k < 11; ++k) {
-        CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
         din[k] = dev_in + (size_t)k * G;
+        if (q_defer && k >= 6 && k <= 9) continue;
+        CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
+      }
+      if (q_defer) {
+        if (!s->qstream) s->qstream = acquire_side_stream(s->device);
+        if (!s->qstream) return fail(LOBE_E_CUDA, "side stream creation failed");
+        CK(s->alloc(&q_flags, 4));
+        const uint32_t qinit[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
+        CK(cudaMemcpyAsync(q_flags, qinit, sizeof(qinit), cudaMemcpyHostToDevice, st));
       }
     } else {
       for (int k = 0; k < 11; ++k) din[k] = src[k];
     }
+    // camera buffers now (stream-ordered allocations a side stream may write)
+    const int64_t NLc = std::max<int64_t>(s->N_loc, 1);
+    float* cr = nullptr;  // camera-centre raw grid coordinates
+    CK(s->alloc(&s->cams, NLc));
+    CK(s->alloc(&s->d_cam_gu, NLc));
+    CK(s->alloc(&s->d_cam_gv, NLc));
+    if (s->aniso) CK(s->alloc(&s->acams, NLc));
+    CK(s->alloc(&cr, (size_t)2 * NLc));
+    if (q_defer) CK(cudaEventRecord(s->ev[20], st));  // the side stream starts after the fields' copies
     // ---- a1 precompute
 
     float4* rec;
@@ -1324,6 +1365,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     pin.rho = F.radius;
     pin.cov = cov_raw;
+    pin.q_deferred = q_defer ? 1 : 0;
     tl.mark("inputs + a1 allocs");
     KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
     tl.mark("k_prep_raw launched");
@@ -1350,6 +1392,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->release(rec);
     s->release(keys); s->release(keys_s); s->release(vals); s->release(perm);
     s->release(err_idx);
+    float* dev_in_q = nullptr;  // deferred path: freed after the quaternion check (below)
+    if (dev_in && q_defer) {
+      dev_in_q = dev_in;
+      dev_in = nullptr;
+    }
     if (dev_in) s->release(dev_in);
 
     // ---- a2 camera setup (local shard) + camera-centre grid coords
@@ -1369,20 +1416,38 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       cam_centre(k, oc);
       ground_uv_host((float)oc[0], (float)oc[1], (float)oc[2], F, &cam_ru[c], &cam_rv[c]);
     }
-    const int64_t NL = std::max<int64_t>(s->N_loc, 1);
-    CK(s->alloc(&s->cams, NL));
-    CK(s->alloc(&s->d_cam_gu, NL));
-    CK(s->alloc(&s->d_cam_gv, NL));
-    CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, st));
-    if (s->aniso) {
-      CK(s->alloc(&s->acams, NL));
-      CK(cudaMemcpyAsync(s->acams, haset.data(), sizeof(AnisoCam) * NL, cudaMemcpyHostToDevice, st));
-    }
+    const int64_t NL = NLc;
+    // with deferred quaternions the H2D engine is shared: the camera copies go
+    // first, on the side stream (the H2D engine serves copies in issue order,
+    // and copies queued on the scene's stream behind k_pack would wait for the
+    // 160 MB of quaternions); the scene's stream waits for them (event 22)
+    cudaStream_t cst = q_defer ? s->qstream : st;
+    if (q_defer) CK(cudaStreamWaitEvent(cst, s->ev[20], 0));
+    CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, cst));
+    if (s->aniso) CK(cudaMemcpyAsync(s->acams, haset.data(), sizeof(AnisoCam) * NL, cudaMemcpyHostToDevice, cst));
     {  // camera-centre grid coordinates, normalised on the device with k_prep_raw's min / max
-      float* cr;
-      CK(s->alloc(&cr, (size_t)2 * NL));
-      CK(cudaMemcpyAsync(cr, cam_ru.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(cr + NL, cam_rv.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(cr, cam_ru.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, cst));
+      CK(cudaMemcpyAsync(cr + NL, cam_rv.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, cst));
+      if (q_defer) {
+        CK(cudaEventRecord(s->ev[22], cst));
+        CK(cudaStreamWaitEvent(st, s->ev[22], 0));
+        // now the quaternions (side stream) and their check
+        for (int k = 6; k <= 9; ++k)
+          CK(cudaMemcpyAsync(dev_in_q + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice,
+                             s->qstream));
+        KL(launch_check_quats(dev_in_q + 6 * (size_t)G, dev_in_q + 7 * (size_t)G, dev_in_q + 8 * (size_t)G,
+                              dev_in_q + 9 * (size_t)G, G, q_flags, reinterpret_cast<unsigned long long*>(q_flags + 2),
+                              s->qstream));
+        CK(cudaMemcpyAsync(&s->pin->q_err, q_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->qstream));
+        CK(cudaMemcpyAsync(&s->pin->q_bad, q_flags + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           s->qstream));
+        CK(cudaEventRecord(s->ev[20], s->qstream));
+        // dev_in is freed on the side stream once both readers are done
+        CK(cudaEventRecord(s->ev[21], st));
+        CK(cudaStreamWaitEvent(s->qstream, s->ev[21], 0));
+        CK(cudaFreeAsync(dev_in_q, s->qstream));
+        CK(cudaFreeAsync(q_flags, s->qstream));
+      }
       if (s->N_loc > 0) KL(launch_cam_grid(s->N_loc, cr, cr + NL, scratch + 1, s->d_cam_gu, s->d_cam_gv, st));
       s->release(cr);
       s->release(scratch);
@@ -1453,7 +1518,11 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->n_units = nu;
     {  // k_prep_raw's verdict (its copies completed with this synchronisation)
       const uint32_t* hs = s->pin->prep_hs;
-      const unsigned long long hbad = s->pin->prep_bad;
+      unsigned long long hbad = s->pin->prep_bad;
+      if ((hs[0] & 1u) && q_defer) {  // report the first invalid Gaussian of either check
+        CK(cudaEventSynchronize(s->ev[20]));
+        if (s->pin->q_err) hbad = std::min(hbad, s->pin->q_bad);
+      }
       if (hs[0] & 1u)
         return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(hbad) +
                                               " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
@@ -1477,14 +1546,13 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->queue, 1));
     if (s->N_loc > 0 && kept_pairs > 0) {
       uint32_t* tlist = nullptr;  // tile of each kept pair (k_slice_codes only)
-      if (!s->aniso) CK(s->alloc(&tlist, (size_t)kept_pairs));
+      CK(s->alloc(&tlist, (size_t)kept_pairs));
       KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, tlist, 1, st));
-      if (!s->aniso) {
-        CK(cudaEventRecord(s->ev[16], st));
-        KL(launch_slice_codes((int64_t)kept_pairs, s->klist, tlist, s->cams, s->slice_lo, s->slice_hi, s->codes, st));
-        CK(cudaEventRecord(s->ev[17], st));
-        s->release(tlist);
-      }
+      CK(cudaEventRecord(s->ev[16], st));
+      KL(launch_slice_codes((int64_t)kept_pairs, s->klist, tlist, s->cams, s->aniso ? s->acams : nullptr,
+                            s->slice_lo, s->slice_hi, s->codes, st));
+      CK(cudaEventRecord(s->ev[17], st));
+      s->release(tlist);
       KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile, nu, 1, st));
     }
     s->release(uc);
@@ -1573,6 +1641,14 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     CK(cudaEventRecord(s->ev[3], st));
     tl.mark("rest enqueued");
+    if (q_defer) {  // the deferred quaternion check decides before the load returns
+      CK(cudaEventSynchronize(s->ev[20]));
+      if (s->pin->q_err)
+        return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(s->pin->q_bad) +
+                                              " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
+                                              "SPEC.md:30-33)");
+      tl.mark("quaternion check");
+    }
     // no synchronisation here: the depth statistic may still run while the caller
     // enqueues the next call; event timings are read lazily (finalize_load_stats)
     s->kept_pairs_last = kept_pairs;

@@ -35,12 +35,17 @@ static_assert(sizeof(PairPartial) == 32, "PairPartial layout");
 
 // Zone tables for one grid (a5): per axis, sorted breakpoints P[0..nz-2] with
 // P[0] = 0; zone z < nz-1 is [P[z], P[z+1]) (P[nz-1] := 1), zone nz-1 is {1}.
+constexpr int kZoneBins = 1024;  // zone lookup bins per axis: bin b = [b / 1024, (b + 1) / 1024)
 struct AxisZones {
   int nz;                      // number of zones including the top zone {1}
   int count;                   // intervals on this axis (m or n)
   float P[kMaxZones];          // breakpoints (nz-1 of them)
   uint8_t cell[kMaxZones];     // delta=0 interval of the zone
   uint64_t encl[kMaxZones];    // bitmask of enlarged intervals containing the zone
+  // zone of x by bin (exact, replaces the binary search): low 12 bits = zone of the
+  // bin's lower end; bits 14-15 = 0: no breakpoint strictly inside the bin, 1: one
+  // (the zone is +1 from it on), 2: several (binary search)
+  uint16_t bin[kZoneBins];
 };
 struct ZoneTables {
   AxisZones U, V;
@@ -53,7 +58,12 @@ struct PrepIn {
   int64_t G;
   float c0[3], rho, au[3], av[3];
   float* cov;  // anisotropic predicate: 6 floats per Gaussian (caller order), else NULL
+  int q_deferred;  // 1: the quaternions are validated by k_check_quats (host inputs, isotropic)
 };
+// |q| = 1 +- 1e-6, the check k_prep_raw applies, for the deferred
+// path: err |= 1 and err_idx = min index of an invalid quaternion
+cudaError_t launch_check_quats(const float* qw, const float* qx, const float* qy, const float* qz, int64_t G,
+                               uint32_t* err, unsigned long long* err_idx, cudaStream_t st);
 
 // Anisotropic predicate (ledger L24): the raw camera parameters of the EWA
 // footprint test, plus w2 >= ||R||_2^2 (host: max absolute row sum of R^T R in
@@ -132,7 +142,8 @@ cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float
 // (0 reject, 2 accept, 1 | need << 2 undecided), so the test kernel loads
 // camera parameters only for undecided slices
 cudaError_t launch_slice_codes(int64_t n_kept, const uint32_t* klist, const uint32_t* tlist, const CamSetup* cams,
-                               const float4* slo, const float4* shi, uint32_t* codes, cudaStream_t st);
+                               const AnisoCam* acams, const float4* slo, const float4* shi, uint32_t* codes,
+                               cudaStream_t st);
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
                               const uint32_t* offs, uint32_t* list, uint32_t* tlist, int phase, cudaStream_t st);
 // tile-major visibility over the kept lists: work units = (tile, <= kVisUnit cameras)

@@ -158,6 +158,19 @@ def test_call_orders(tiny_scene):
     assert (crop == o["crop"]).all() and (elig == o["eligible"]).all()
 
 
+def test_zone_bins_dense_and_aligned_cuts():
+    """The zone lookup bins (1/1024 wide): three cuts inside one bin (binary-search
+    fallback), cuts exactly on bin edges (0.25, 0.5, 0.75) and a point-dense
+    scene, with and without enlargement: counts, assignment, loads and masks
+    stay bit-exact."""
+    sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x5151))
+    v = np.array([0.3, 0.3001, 0.3002], np.float32)
+    h = np.array([0.25, 0.5, 0.75], np.float32)
+    full_parity(sc, [oracle.default_grid(4, 4, v=v, h=h), oracle.default_grid(4, 4, v=v, h=h, delta_v=0.0,
+                                                                               delta_h=0.0),
+                     oracle.default_grid(4, 4, v=h, h=v, delta_v=0.0001, delta_h=0.25)])
+
+
 def test_mid_size():
     sc = make_scene(make_config("matrixcity", G=150_000, N=120, seed=0x77))
     full_parity(sc, [oracle.default_grid(6, 6), _rand_grid(5, 4, 9)])
@@ -361,6 +374,40 @@ def test_invalid_camera_gpu():
             lobe.Scene(sc, bad)
         assert e.value.status == "INVALID_INPUT", field
     with lobe.Scene(sc, sc) as S:  # the valid scene still loads afterwards
+        assert S.assign_cameras(2, 2)["K"].sum() > 0
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+@pytest.mark.parametrize("predicate", [0, 1])
+def test_invalid_gaussians_gpu(on_device, predicate):
+    """Every Gaussian field is validated (O1) whichever path the
+    inputs take -- host inputs in the isotropic mode validate the quaternions
+    on a side stream after the other fields -- and the message names the first
+    invalid Gaussian, as the oracle does."""
+    import torch
+    lobe = _lobe()
+    cases = [(("qw", 700, 0.5),), (("sx", 900, -1.0), ("qx", 700, 3.0)), (("qy", 900, np.nan), ("opacity", 700, 1.5)),
+             (("x", 10, np.inf),), (("qz", 9999, 0.9),)]
+    for changes in cases:
+        bad = make_scene("tiny")
+        for field, idx, val in changes:
+            getattr(bad, field)[idx] = val
+        with pytest.raises(oracle.OracleError) as eo:
+            oracle.validate(bad)
+        first = min(idx for _, idx, _ in changes)
+        assert f"index {first}" in str(eo.value)
+        g = bad
+        if on_device:
+            class DG:
+                pass
+            g = DG()
+            for k in ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity"):
+                setattr(g, k, torch.from_numpy(getattr(bad, k)).cuda())
+        with pytest.raises(lobe.LobeError) as e:
+            lobe.Scene(g, bad, predicate=predicate)
+        assert e.value.status == "INVALID_INPUT" and f"gaussian {first} " in str(e.value), (changes, str(e.value))
+    sc = make_scene("tiny")
+    with lobe.Scene(sc, sc, predicate=predicate) as S:  # valid inputs still load
         assert S.assign_cameras(2, 2)["K"].sum() > 0
 
 
