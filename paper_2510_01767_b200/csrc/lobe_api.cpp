@@ -781,7 +781,8 @@ lobe_status scratch(lobe_scene* s, RenderJob& J, int k, T** out, size_t count) {
   RenderJob::Buf& b = J.b[k];
   if (b.cap < bytes) {
     // 1.5x headroom: later batches rarely need a new block. Plain cudaMalloc:
-    // these multi-GB blocks would otherwise grow the stream-ordered pool (slow)
+    // growing the stream-ordered pool by these multi-GB blocks is far slower
+    // (measured: 1.1 s of cudaMallocAsync per MatrixCity render selection)
     const size_t cap = std::max(bytes, b.cap * 3 / 2);
     if (b.p) {
       CK(cudaStreamSynchronize(s->stream));
@@ -889,18 +890,31 @@ lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<ui
   TRY(scratch(s, J, 8, &rec, N1 * 10));
   TRY(scratch(s, J, 9, &dseg, (size_t)ncam + 1));
   CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(uint32_t) * (ncam + 1), cudaMemcpyHostToDevice, st));
+  // depth key bits: every splat's zc lies in (z_near, z_far) of its camera, so
+  // zc bits - (the batch's smallest z_near bits) fit in zb bits (27 at the
+  // synthetic configs' 0.01 .. 8 instead of 32: one radix pass less)
+  uint32_t zlo = 0xFFFFFFFFu, zhi = 0u;
+  for (int q = 0; q < ncam; ++q) {
+    uint32_t a, b;
+    std::memcpy(&a, &hcams[c0 + q].z_near, 4);
+    std::memcpy(&b, &hcams[c0 + q].z_far, 4);
+    zlo = std::min(zlo, a);
+    zhi = std::max(zhi, b);
+  }
+  int zb = 1;
+  while (zb < 32 && (1ull << zb) <= (unsigned long long)(zhi - zlo)) ++zb;
   KL(launch_rvis_fill(k0, nk, (int)c0, s->cam_order, s->pair_tile, s->pair_cam, s->rows, s->words, pos, prec, drc,
-                      keys, vals, rec, rcam, st));
+                      zlo, zb, keys, vals, rec, rcam, st));
   // 2. front to back per camera: (zc, caller index) -- one radix sort on
   //    (camera, zc bits), then runs of equal depth ordered by caller index
   if (n > 0) {
     int cb = 1;
     while ((1 << cb) < ncam) ++cb;
     size_t tb = 0;
-    CK(sort_u64_pairs(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, 32 + cb, st));
+    CK(sort_u64_pairs(nullptr, tb, keys, keys_s, vals, vals_s, (int64_t)n, zb + cb, st));
     uint8_t* tmp = nullptr;
     TRY(scratch(s, J, 10, &tmp, tb));
-    CUBL(sort_u64_pairs(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, 32 + cb, st));
+    CUBL(sort_u64_pairs(tmp, tb, keys, keys_s, vals, vals_s, (int64_t)n, zb + cb, st));
     KL(launch_tie_fix((int64_t)n, keys_s, vals_s, rec, st));
   }
   // 3. tile binning in front-to-back order (stable key sort keeps it)

@@ -271,8 +271,8 @@ cudaError_t launch_rvis_count(int64_t k0, int64_t nk, const int32_t* cam_order, 
                               cudaStream_t st);
 cudaError_t launch_rvis_fill(int64_t k0, int64_t nk, int c0, const int32_t* cam_order, const uint32_t* pair_tile,
                              const uint32_t* pair_cam, const uint32_t* rows, int64_t words, const uint32_t* pos,
-                             const float4* prec, const RenderCam* rc, unsigned long long* keys, uint32_t* vals,
-                             float* rec, uint32_t* rcam, cudaStream_t st);
+                             const float4* prec, const RenderCam* rc, uint32_t zlo, int zb, unsigned long long* keys,
+                             uint32_t* vals, float* rec, uint32_t* rcam, cudaStream_t st);
 cudaError_t launch_render_prep(int64_t G, const int32_t* perm, const SubArgs& g, float4* prec, cudaStream_t st);
 cudaError_t seg_sort_u64(void* tmp, size_t& tmp_bytes, const unsigned long long* kin, unsigned long long* kout,
                          const uint32_t* vin, uint32_t* vout, int64_t n, int nseg, const uint32_t* seg_begin,
