@@ -1399,7 +1399,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
     CK(s->alloc(&s->iperm, (size_t)G));
     if (s->aniso) CK(s->alloc(&s->cv, (size_t)s->G_pad / 2 * 3));
-    KL(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st));
+    KLN(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st), 2);
     tl.mark("sort + k_pack launched");
     s->release(cov_raw);
     cudaFreeAsync(tmp, st);
