@@ -310,12 +310,20 @@ def main():
         return run_reference(args, cfg_name)
     import torch
     import torch.distributed as dist
-    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
-        sys.stderr.write(f"bench.py: rank {rank} needs GPU {local}; {torch.cuda.device_count()} visible\n")
+    # LOBE_BENCH_SHARED_GPU=1 (tests only): every rank on GPU 0 with a gloo group,
+    # so the library's host-callback communicator carries the exchange -- checks
+    # the multi-rank plumbing of this script on a one-GPU box; never a bench value
+    shared = os.environ.get("LOBE_BENCH_SHARED_GPU") == "1"
+    dev = 0 if shared else local
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= dev:
+        sys.stderr.write(f"bench.py: rank {rank} needs GPU {dev}; {torch.cuda.device_count()} visible\n")
         return 2
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2510_01767_b200 import lobe
     from paper_2510_01767_b200.engine import Engine, shard
     from synth import make_scene
@@ -562,7 +570,9 @@ def main():
     line = {"metric": "gaussian_camera_visibility_tests_per_s", "value": value, "unit": "tests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config_dict(cfg_name, sc, pred, world),
+            "data": "synthetic" + (" (LOBE_BENCH_SHARED_GPU test run: all ranks on GPU 0, not a measurement)"
+                                   if shared else ""),
+            "config": config_dict(cfg_name, sc, pred, world),
             "roofline": roof, "depth_roofline": depth_roof, "evaluation_roofline": evaluation,
             # the scaling quantity (a3 + a5-a8 + combine, max over ranks) and the exchange alone
             "engine_eval_ms": engine_eval_max, "t_comm_ms": t_comm, "t_vis_ms_max_over_ranks": t_vis,

@@ -123,3 +123,29 @@ def test_host_comm_ranks_match_world1(world):
         _same(out, ref)
     for p in procs:
         assert p.exitcode == 0
+
+
+def test_bench_two_ranks_shared_gpu():
+    """bench.py's multi-rank path (self-spawn under torch.distributed.run, the
+    collective engine, timings max over ranks, rank-0 line) with both ranks on
+    the one GPU through the host-callback communicator (LOBE_BENCH_SHARED_GPU):
+    the line reports 2 GPUs and the world-1 objective."""
+    import json
+    import subprocess
+    import sys
+    _lobe()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = [sys.executable, os.path.join(root, "bench.py"), "--config", "tiny", "--steps", "2", "--warmup", "3",
+            "--no-bo", "--no-cpu-baseline", "--no-dense-ref", "--e2e-steps", "1", "--render", "0"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    one = subprocess.run(args, cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert one.returncode == 0, one.stderr[-2000:]
+    l1 = json.loads(one.stdout.strip().splitlines()[-1])
+    env["LOBE_BENCH_SHARED_GPU"] = "1"
+    two = subprocess.run(args + ["--gpus", "2"], cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert two.returncode == 0, two.stderr[-3000:]
+    l2 = json.loads([l for l in two.stdout.splitlines() if l.startswith("{")][-1])
+    assert l2["n_gpus"] == 2 and l2["value"] > 0 and l2["engine_eval_ms"] > 0
+    assert l2["objective_uniform"] == l1["objective_uniform"]
+    assert l2["visible_incidences"] == l1["visible_incidences"]
+    assert "not a measurement" in l2["data"]
