@@ -2,8 +2,9 @@
 is the objective), at the BASELINE configs' full sizes and in the launch
 configuration bench.py times.
 
-- Rubble-, Building- and Residence-shaped: the oracle runs live on the host
-  cores (tens of seconds each) and every output is compared element by element:
+- Rubble-, Building- and Residence-shaped (and Rubble in the anisotropic
+  mode): the oracle runs live on the host cores (tens of seconds each) and
+  every output is compared element by element:
   rows of all cameras, K, D_c (1e-6 relative), z_min, z_max, n, n0, member, home,
   all block records, crop and eligible masks, on the uniform cuts and a second
   grid with non-uniform cuts and tau = 0.3.
@@ -40,6 +41,14 @@ def _grids(m, n):
 def test_fullsize_live_oracle(name):
     sc = make_scene(name)
     full_parity(sc, _grids(sc.cfg.m, sc.cfg.n))
+
+
+def test_fullsize_live_oracle_aniso_rubble():
+    """The anisotropic (EWA) predicate mode at the full Rubble-shaped size: every
+    output against the oracle's O6a, element by element (~30 s of oracle on
+    16 cores)."""
+    sc = make_scene("rubble")
+    full_parity(sc, _grids(sc.cfg.m, sc.cfg.n), predicate=1)
 
 
 def _sha(a):
