@@ -236,9 +236,14 @@ typedef struct {
 /* Validate, resolve the frame, precompute per-Gaussian data (contraction,
  * grid coords, footprint radius, opacity gate, spatial sort) and per-camera
  * projection rows, then run the visibility pass once for the local cameras
- * (rows, K_c, depth sums). Everything after this reuses the cached rows
- * ("the back-projection is computed once and reused").
- * inout_frame may be NULL (= LOBE_FRAME_AUTO_ALL). */
+ * (rows). Everything after this reuses the cached rows ("the back-projection
+ * is computed once and reused"); the depth statistic (K_c, D_c,
+ * z_min, z_max) is enqueued after the first crop kernel or by the first call
+ * that needs it. Every input is validated before the call returns (host inputs
+ * in the isotropic mode: the quaternions are copied last, on a side stream,
+ * with their own check; the error names the first invalid Gaussian either
+ * way). With a communicator this call is collective (NCCL communicators are
+ * created here on first use). inout_frame may be NULL (= LOBE_FRAME_AUTO_ALL). */
 lobe_status lobe_load_scene(const lobe_gaussians* gaussians, const lobe_camera* cameras, int64_t n_cams,
                             lobe_frame* inout_frame, const lobe_options* options, lobe_scene** out);
 void lobe_free_scene(lobe_scene* scene);
