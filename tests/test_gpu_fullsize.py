@@ -43,6 +43,23 @@ def test_fullsize_live_oracle(name):
     full_parity(sc, _grids(sc.cfg.m, sc.cfg.n))
 
 
+def test_fullsize_bo_trajectory_rubble():
+    """a10 at full Rubble size: every evaluation of lobe_balance_partition (L = 8:
+    the uniform cuts, Sobol points, then GP + EI proposals) equals the oracle's
+    objective at the recorded cuts, so an oracle-backed BO follows the same
+    trajectory."""
+    lobe = _lobe()
+    sc = make_scene("rubble")
+    m, n = sc.cfg.m, sc.cfg.n
+    o = oracle.run(sc, masks=False)
+    with lobe.Scene(sc, sc) as S:
+        r = S.balance_partition(m, n, L=8, seed=2)
+    for row, val in zip(r["cut_history"], r["history"]):
+        g = oracle.default_grid(m, n, v=row[:m - 1], h=row[m - 1:])
+        assert oracle.evaluate_cuts(sc, o["pre"], o["vis"], g) == val
+    assert r["best"]["objective"] == r["history"].min() <= r["history"][0]
+
+
 def test_fullsize_live_oracle_aniso_rubble():
     """The anisotropic (EWA) predicate mode at the full Rubble-shaped size: every
     output against the oracle's O6a, element by element (~30 s of oracle on
