@@ -258,6 +258,35 @@ def test_determinism_and_permutation(tiny_scene):
         assert (ub == ua[:, perm]).all()
 
 
+def test_camera_order_invariance_and_duplicates_gpu():
+    """I14: permuting the cameras permutes every per-camera output and leaves the
+    block loads and masks unchanged; P6: a duplicated camera gets identical rows
+    and per-camera outputs."""
+    lobe = _lobe()
+    sc = make_scene(make_config("residence", G=37_123, N=53, seed=0x5151))
+    perm = np.random.default_rng(5).permutation(sc.N)
+    sp = sc.subset_cameras(perm)
+    with lobe.Scene(sc, sc) as A, lobe.Scene(sp, sp) as Bs:
+        for m, n in ((4, 4), (3, 2)):
+            la, lb = A.block_loads(m, n), Bs.block_loads(m, n)
+            for k in ("n_cams", "g_vis", "g_blk", "incidences", "g_avgvis", "area", "lohi"):
+                assert (la[k] == lb[k]).all(), k
+            ca, ea = A.crop_masks(m, n)
+            cb, eb = Bs.crop_masks(m, n)
+            assert (ca == cb).all() and (ea == eb).all()
+            aa, ab = A.assign_cameras(m, n), Bs.assign_cameras(m, n)
+            for k in aa:
+                assert (aa[k][perm] == ab[k]).all(), k
+        assert (A.export_rows()[perm] == Bs.export_rows()).all()
+    dup = sc.subset_cameras(np.r_[np.arange(sc.N), [7, 7]])
+    with lobe.Scene(dup, dup) as D:
+        rows = D.export_rows()
+        assert (rows[7] == rows[sc.N]).all() and (rows[7] == rows[sc.N + 1]).all()
+        a = D.assign_cameras(4, 4)
+        for k in a:
+            assert (a[k][7] == a[k][sc.N]).all(), k
+
+
 def test_world_shards_match_world1():
     """Camera sharding on one GPU, ranks run one after another:
     per-camera outputs concatenate, OR-combined partial masks equal world=1."""
