@@ -468,13 +468,25 @@ def main():
             barrier()
             rs = time.perf_counter() - t0
             off, _, _ = eng.local.camera_clouds()
+            rst = eng.stats()
+            rflop = 11.0 * rst.render_tests + 28.0 * rst.render_composited
             t0 = time.perf_counter()
             r2 = eng.balance_partition(m, n, L=args.bo_L, seed=0)
             bo2 = time.perf_counter() - t0
             bo["render_selection"] = {"seconds": rs, "cameras": int(N), "cloud_points": int(off[-1]),
                                       "downscale": 4, "stride": 2, "eps_w": 0.1,
                                       "bo_seconds": bo2, "objective_uniform": int(r2["history"][0]),
-                                      "objective_best": int(r2["history"].min())}
+                                      "objective_best": int(r2["history"].min()),
+                                      # k_render (per-pixel compositing): 11 flop per (pixel, splat) footprint
+                                      # test + 28 per composited splat (pinned exp, alpha, weights, depth)
+                                      "k_render": {"ms": rst.t_render_kernel_ms, "tests": int(rst.render_tests),
+                                                   "composited": int(rst.render_composited), "flop": rflop,
+                                                   "achieved_TFLOPs": rflop / max(rst.t_render_kernel_ms, 1e-9)
+                                                   * 1e-9,
+                                                   "frac_fp32": rflop / max(rst.t_render_kernel_ms, 1e-9) * 1e-9
+                                                   / (torch.cuda.get_device_properties(0).multi_processor_count
+                                                      * FP32_LANES_PER_SM * 2 * 1.965e9 / 1e12),
+                                                   "bound": "alu (compositing loop; splats staged in shared memory)"}}
         eng.close()
 
     cpu = None

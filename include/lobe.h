@@ -229,6 +229,9 @@ typedef struct {
   uint64_t exact_pattern_tests[9]; /* isotropic exact tests by open-condition pattern (k_vis_tiles): left, top,
                                       right, bottom edge; top-left, top-right, bottom-left corner; the four edges;
                                       all six -- 3, 3, 7, 7, 6, 10, 10, 11, 11 FFMA per test (issued flop) */
+  uint64_t render_tests;      /* last lobe_render_select: (pixel, splat) footprint tests in k_render (11 flop each) */
+  uint64_t render_composited; /* ... of which composited (inside the 3-sigma ellipse: + 28 flop incl. the pinned exp) */
+  double t_render_kernel_ms;  /* ... k_render's CUDA-event time summed over the batches */
 } lobe_stats;
 
 /* ---- scene --------------------------------------------------------------- */

@@ -766,6 +766,9 @@ struct RenderJob {
   int64_t n = 0, cap = 0;
   // optional: maps of the batch's first camera copied here (host or device)
   float *Dout = nullptr, *Wout = nullptr;
+  // k_render roofline: (pixel, splat) tests / composited (device counters), kernel time
+  unsigned long long* counters = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;  // around each batch's k_render
   // grow-only scratch reused by every batch (no pool growth between batches)
   struct Buf {
     void* p = nullptr;
@@ -949,7 +952,13 @@ lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<ui
   float *Dm = nullptr, *Wm = nullptr;
   TRY(scratch(s, J, 17, &Dm, (size_t)std::max<int64_t>(maps, 1)));
   TRY(scratch(s, J, 18, &Wm, (size_t)std::max<int64_t>(maps, 1)));
-  KL(launch_render(ncam, max_tiles, drc, ts, te, ev_s, rec, Dm, Wm, st));
+  std::pair<cudaEvent_t, cudaEvent_t> ke{nullptr, nullptr};
+  if (J.counters && cudaEventCreate(&ke.first) == cudaSuccess && cudaEventCreate(&ke.second) == cudaSuccess) {
+    J.kev.push_back(ke);
+    CK(cudaEventRecord(ke.first, st));
+  }
+  KL(launch_render(ncam, max_tiles, drc, ts, te, ev_s, rec, Dm, Wm, J.counters, st));
+  if (ke.second) CK(cudaEventRecord(ke.second, st));
   if (J.Dout) TRY(copy_out(s, J.Dout, Dm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
   if (J.Wout) TRY(copy_out(s, J.Wout, Wm, sizeof(float) * (size_t)rc[0].Wd * rc[0].Hd));
   // 5. back-projection of every stride-th pixel with weight >= eps_w
@@ -2198,7 +2207,23 @@ lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int3
   J.stride = stride <= 0 ? 2 : stride;
   J.eps_w = eps_w < 0.0f ? 0.1f : eps_w;
   std::vector<uint32_t> counts;
+  CK(s->alloc(&J.counters, 2));
+  CK(cudaMemsetAsync(J.counters, 0, 2 * sizeof(unsigned long long), s->stream));
   lobe_status rs = render_cameras(s, coarse, 0, s->N_loc, J, &counts);
+  {  // k_render roofline counters and kernel time (render_cameras ended with a sync)
+    unsigned long long hc[2] = {0, 0};
+    cudaMemcpy(hc, J.counters, sizeof(hc), cudaMemcpyDeviceToHost);
+    double ms = 0.0;
+    for (auto& e : J.kev) {
+      ms += ms_between(e.first, e.second);
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    s->st.render_tests = hc[0];
+    s->st.render_composited = hc[1];
+    s->st.t_render_kernel_ms = ms;
+    s->release(J.counters);
+  }
   if (rs != LOBE_OK) {
     s->release(J.gu); s->release(J.gv); s->release(J.cam);
     return rs;

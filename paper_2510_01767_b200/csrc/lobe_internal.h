@@ -288,7 +288,8 @@ cudaError_t launch_bin_fill(int64_t n, const uint32_t* svals, const float* rec, 
                             const RenderCam* rc, const uint32_t* off, uint32_t* ekey, uint32_t* eval, cudaStream_t st);
 cudaError_t launch_tile_ranges(int64_t n, const uint32_t* skey, uint32_t* start, uint32_t* end, cudaStream_t st);
 cudaError_t launch_render(int ncam, int max_tiles, const RenderCam* rc, const uint32_t* start, const uint32_t* end,
-                          const uint32_t* sval, const float* rec, float* Dmap, float* Wmap, cudaStream_t st);
+                          const uint32_t* sval, const float* rec, float* Dmap, float* Wmap,
+                          unsigned long long* counters, cudaStream_t st);
 cudaError_t launch_bp_count(int ncam, int max_samples, const RenderCam* rc, int stride, float eps_w, const float* Wmap,
                             const uint32_t* sp0, uint32_t* flag, cudaStream_t st);
 cudaError_t launch_bp_write(int ncam, int max_samples, const RenderCam* rc, int stride, const float* Dmap,

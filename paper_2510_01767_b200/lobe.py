@@ -131,7 +131,8 @@ class Stats(ctypes.Structure):
                 ("cub_launches", ctypes.c_uint64), ("kept_tests", ctypes.c_uint64),
                 ("accepted_tests", ctypes.c_uint64), ("exact_variant_tests", ctypes.c_uint64 * 6),
                 ("decided_tests", ctypes.c_uint64 * 4), ("visible_bits", ctypes.c_uint64 * 2),
-                ("exact_pattern_tests", ctypes.c_uint64 * 9)]
+                ("exact_pattern_tests", ctypes.c_uint64 * 9), ("render_tests", ctypes.c_uint64),
+                ("render_composited", ctypes.c_uint64), ("t_render_kernel_ms", ctypes.c_double)]
 
 
 OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
