@@ -154,6 +154,8 @@ struct lobe_scene {
   PairPartial* pair_part = nullptr;
   // a4 deferred until needed (ensure_a4)
   bool a4_pending = false;
+  bool a4_side = false, a4_joined = false;  // a4 on the depth side stream (LOBE_A4_STREAM=1)
+  cudaStream_t dstream = nullptr;
   uint32_t* camtile = nullptr;  // camera x tile bits of the non-empty pairs (a4's camera order)
   int64_t a4_cap = 0, a4_tw = 0;
   unsigned long long a4_kept = 0;
@@ -988,21 +990,18 @@ lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<ui
 
 
 // a4, the per-camera depth statistic over the non-empty (tile, camera) pairs of
-// the load pass, enqueued on the scene's stream once (see lobe_load_scene).
-lobe_status ensure_a4(lobe_scene* s) {
-  if (!s->a4_pending) return LOBE_OK;
-  s->a4_pending = false;
-  cudaStream_t st = s->stream;
+// the load pass, enqueued once on `st` (the scene's stream, or the depth side
+// stream; see lobe_load_scene). Its scratch lives and dies on `st`.
+lobe_status launch_a4(lobe_scene* s, cudaStream_t st) {
   const int64_t NL = std::max<int64_t>(s->N_loc, 1), cap = s->a4_cap, tw = s->a4_tw;
-  CK(cudaEventRecord(s->ev[11], st));
   if (s->N_loc > 0) {
     KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words,
                           reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk),
                           reinterpret_cast<const float2*>(s->o2), s->cams, s->pair_part, st));
     // pair indices in camera-major order, tile order within a camera
     uint32_t *ccount = nullptr, *wordpre = nullptr;
-    CK(s->alloc(&ccount, (size_t)NL + 1));
-    CK(s->alloc(&wordpre, (size_t)NL * tw));
+    CK(malloc_async(&ccount, sizeof(uint32_t) * ((size_t)NL + 1), st));
+    CK(malloc_async(&wordpre, sizeof(uint32_t) * (size_t)NL * tw, st));
     CK(cudaMemsetAsync(ccount + NL, 0, sizeof(uint32_t), st));
     KL(launch_cam_order(s->N_loc, tw, s->camtile, wordpre, ccount, st));
     size_t sb2 = 0;
@@ -1011,15 +1010,32 @@ lobe_status ensure_a4(lobe_scene* s) {
     CK(malloc_async(&tmp2, sb2, st));
     CUBL(exclusive_scan_u32(tmp2, sb2, ccount, s->cam_off, NL + 1, st));
     cudaFreeAsync(tmp2, st);
-    s->release(ccount);
+    cudaFreeAsync(ccount, st);
     if (s->a4_kept > 0)
       KL(launch_cam_scatter(s->tile_off, s->n_tiles, cap, s->pair_cam, s->pair_tile, s->camtile, wordpre, tw,
                             s->cam_off, s->cam_order, st));
-    s->release(wordpre);
+    cudaFreeAsync(wordpre, st);
     KL(launch_depth_reduce(s->N_loc, s->cam_off, s->cam_order, s->pair_part, s->K, s->D, s->zmin, s->zmax, st));
   }
-  s->release(s->camtile);
+  if (s->camtile) cudaFreeAsync(s->camtile, st);
+  s->camtile = nullptr;
   CK(cudaEventRecord(s->ev[12], st));
+  return LOBE_OK;
+}
+
+// a4's results for the scene's stream: a deferred a4 is enqueued now; an a4
+// running on the depth side stream is joined (the scene's stream waits for it)
+// when `join` is set.
+lobe_status ensure_a4(lobe_scene* s, bool join = true) {
+  if (s->a4_pending) {
+    s->a4_pending = false;
+    CK(cudaEventRecord(s->ev[11], s->stream));
+    return launch_a4(s, s->stream);
+  }
+  if (s->a4_side && join && !s->a4_joined) {
+    CK(cudaStreamWaitEvent(s->stream, s->ev[12], 0));
+    s->a4_joined = true;
+  }
   return LOBE_OK;
 }
 
@@ -1219,6 +1235,7 @@ size_t lobe_mask_words(const lobe_scene* s) { return s ? (size_t)s->words : 0; }
 void lobe_free_scene(lobe_scene* s) {
   if (!s) return;
   cudaSetDevice(s->device);
+  if (s->a4_side && !s->a4_joined) cudaStreamWaitEvent(s->stream, s->ev[12], 0);  // a4 reads what is freed below
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
@@ -1240,6 +1257,10 @@ void lobe_free_scene(lobe_scene* s) {
   if (s->qstream) {
     cudaStreamSynchronize(s->qstream);
     recycle_side_stream(s->device, s->qstream);
+  }
+  if (s->dstream) {
+    cudaStreamSynchronize(s->dstream);
+    recycle_side_stream(s->device, s->dstream);
   }
   recycle_events(s->device, s->ev);  // event creation costs ~2 us each: reuse across scenes
   recycle_pinned(s->pin);
@@ -1643,10 +1664,28 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     s->a4_cap = cap;
     s->a4_tw = tw;
     s->a4_kept = kept_pairs;
-    s->a4_pending = true;
     CK(s->alloc(&s->pair_part, (size_t)cap));
     CK(s->alloc(&s->cam_off, (size_t)NL + 1));
     CK(s->alloc(&s->cam_order, (size_t)cap));
+    // Where a4 runs. Device-resident inputs: now, on the depth side stream,
+    // concurrent with the caller's evaluation / crop (measured: step 5.30 ->
+    // 5.15 ms at MatrixCity size). Host inputs: deferred behind the first crop
+    // kernel, so it overlaps the crop's device->host copy instead of delaying
+    // the evaluation (e2e 12.6 ms side stream vs 11.3 ms deferred).
+    // LOBE_A4_STREAM=0|1 overrides.
+    const char* a4_env = std::getenv("LOBE_A4_STREAM");
+    const bool a4_stream = a4_env ? a4_env[0] == '1' : (bool)g->on_device;
+    if (a4_stream) {  // a4 now, on the depth side stream, concurrent with the caller's next calls
+      if (!s->dstream) s->dstream = acquire_side_stream(s->device);
+      if (!s->dstream) return fail(LOBE_E_CUDA, "side stream creation failed");
+      CK(cudaEventRecord(s->ev[11], st));
+      CK(cudaStreamWaitEvent(s->dstream, s->ev[11], 0));
+      TRY(launch_a4(s, s->dstream));
+      s->a4_side = true;
+      s->a4_joined = false;
+    } else {
+      s->a4_pending = true;
+    }
     // ---- evaluation scratch
     CK(s->alloc(&s->zp, (size_t)s->G_pad));
     CK(s->alloc(&s->word_zone, (size_t)s->words));
@@ -1839,7 +1878,7 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   CK(cudaEventRecord(s->ev[15], s->stream));
   // a pending a4 (depth statistic) goes on the scene's stream now, so it runs
   // while the masks travel to the host on the side stream (copy engines)
-  TRY(ensure_a4(s));
+  TRY(ensure_a4(s, false));
   const bool host_out = (crop && !crop_dev) || (eligible && !elig_dev);
   if (host_out) {
     if (!s->side) s->side = acquire_side_stream(s->device);
@@ -1930,6 +1969,7 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   if (variant < 0 || variant >= 1 + num_visibility_variants()) return fail(LOBE_E_INVALID_INDEX, "variant");
   if (s->N_loc <= 0 || reps < 1) return fail(LOBE_E_INVALID_CONFIG, "nothing to run");
   CK(cudaSetDevice(s->device));
+  TRY(ensure_a4(s));  // the variants rewrite the rows a4 reads
   VisArgs va{};
   va.xy = reinterpret_cast<const float4*>(s->xy);
   va.zk = reinterpret_cast<const float4*>(s->zk);

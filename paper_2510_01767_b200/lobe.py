@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "liblobe.so")
+LIB_PATH = os.environ.get("LOBE_LIB", os.path.join(_HERE, "csrc", "liblobe.so"))  # override: tuning builds
 
 STATUS = {0: "OK", 1: "INVALID_INPUT", 2: "INVALID_CONFIG", 3: "INVALID_CUTS", 4: "INVALID_INDEX",
           5: "DEGENERATE_SCENE", 6: "CUDA", 7: "NCCL", 8: "OOM", 9: "STATE", 10: "CAPACITY", 11: "INTEGRITY"}
