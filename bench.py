@@ -304,7 +304,8 @@ def main():
         return rc
     rank, world, local = dist_env()
     if args.spawn_check:
-        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        # one write() per line: the ranks share the launcher's stdout pipe
+        os.write(1, (json.dumps({"rank": rank, "world": world, "local_rank": local}) + "\n").encode())
         return 0
     if args.impl == "reference":
         return run_reference(args, cfg_name)

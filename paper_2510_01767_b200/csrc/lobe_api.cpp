@@ -992,12 +992,23 @@ lobe_status render_batch(lobe_scene* s, const float4* prec, const std::vector<ui
 // a4, the per-camera depth statistic over the non-empty (tile, camera) pairs of
 // the load pass, enqueued once on `st` (the scene's stream, or the depth side
 // stream; see lobe_load_scene). Its scratch lives and dies on `st`.
+// CTAs per SM of k_depth_pairs when it runs on the depth side stream next to the
+// evaluation / crop kernels (LOBE_A4_CTAS overrides; 0 = full occupancy, two waves)
+static int a4_side_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("LOBE_A4_CTAS");
+    return e ? std::atoi(e) : 3;
+  }();
+  return v;
+}
+
 lobe_status launch_a4(lobe_scene* s, cudaStream_t st) {
   const int64_t NL = std::max<int64_t>(s->N_loc, 1), cap = s->a4_cap, tw = s->a4_tw;
   if (s->N_loc > 0) {
     KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words,
                           reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk),
-                          reinterpret_cast<const float2*>(s->o2), s->cams, s->pair_part, st));
+                          reinterpret_cast<const float2*>(s->o2), s->cams, s->pair_part,
+                          st == s->dstream ? a4_side_ctas() : 0, s->queue + 1, st));
     // pair indices in camera-major order, tile order within a camera
     uint32_t *ccount = nullptr, *wordpre = nullptr;
     CK(malloc_async(&ccount, sizeof(uint32_t) * ((size_t)NL + 1), st));
@@ -1587,7 +1598,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->codes, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
     CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
-    CK(s->alloc(&s->queue, 1));
+    CK(s->alloc(&s->queue, 2));  // [0] visibility items, [1] a4 tiles (side stream)
     if (s->N_loc > 0 && kept_pairs > 0) {
       uint32_t* tlist = nullptr;  // tile of each kept pair (k_slice_codes only)
       CK(s->alloc(&tlist, (size_t)kept_pairs));

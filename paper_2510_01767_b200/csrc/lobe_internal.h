@@ -158,7 +158,8 @@ cudaError_t launch_visibility_variant(int variant, const VisArgs& a, int num_sms
 // a4: depth statistic per non-empty (tile, camera) pair, then per camera in tile order.
 cudaError_t launch_depth_pairs(int64_t n_tiles, const uint32_t* tile_off, const uint32_t* pair_cam,
                                const uint32_t* rows, int64_t words, const float4* xy, const float4* zk,
-                               const float2* o2, const CamSetup* cams, PairPartial* out, cudaStream_t st);
+                               const float2* o2, const CamSetup* cams, PairPartial* out, int ctas_per_sm,
+                               unsigned long long* tile_queue, cudaStream_t st);
 cudaError_t launch_cam_counts(int64_t n_pairs, const uint32_t* pair_cam, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_iota(int32_t* v, int64_t n, cudaStream_t st);
 cudaError_t launch_depth_reduce(int64_t n_cams, const uint32_t* cam_off, const int32_t* order, const PairPartial* part,
