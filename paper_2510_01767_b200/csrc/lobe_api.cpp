@@ -173,6 +173,7 @@ struct lobe_scene {
   uint32_t* keep = nullptr;
   unsigned long long* kept = nullptr;
   uint32_t *koff = nullptr, *klist = nullptr, *unit_tile = nullptr;
+  uint32_t* unit_meta = nullptr;  // per visibility unit: {tile, first kept pair, cameras, 0}
   int64_t n_units = 0;
   unsigned long long* queue = nullptr;
   int64_t n_sub = 0;
@@ -1251,7 +1252,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
   s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
-  s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->queue); s->release(s->K); s->release(s->D);
+  s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->unit_meta); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
   s->release(s->zp_count); s->release(s->dz); s->release(s->d_zp_cell); s->release(s->hist);
@@ -1553,7 +1554,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&uc, (size_t)s->n_tiles + 1));
     CK(s->alloc(&uoff, (size_t)s->n_tiles + 1));
     CK(cudaMemsetAsync(uc, 0, sizeof(uint32_t) * (s->n_tiles + 1), st));
-    KL(launch_units(s->koff, s->n_tiles, kVisUnit, uc, nullptr, nullptr, 0, 0, st));
+    KL(launch_units(s->koff, s->n_tiles, kVisUnit, uc, nullptr, nullptr, nullptr, 0, 0, st));
     {
       size_t sbu = 0;
       CK(exclusive_scan_u32(nullptr, sbu, uc, uoff, s->n_tiles + 1, st));
@@ -1598,17 +1599,16 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->codes, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
     CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
+    CK(s->alloc(&s->unit_meta, (size_t)4 * std::max<uint32_t>(nu, 1)));
     CK(s->alloc(&s->queue, 2));  // [0] visibility items, [1] a4 tiles (side stream)
     if (s->N_loc > 0 && kept_pairs > 0) {
-      uint32_t* tlist = nullptr;  // tile of each kept pair (k_slice_codes only)
-      CK(s->alloc(&tlist, (size_t)kept_pairs));
-      KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, tlist, 1, st));
+      KL(launch_keep_lists(s->keep, s->n_tiles, s->n_sub, nullptr, s->koff, s->klist, nullptr, 1, st));
+      KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile,
+                       reinterpret_cast<uint4*>(s->unit_meta), nu, 1, st));
       CK(cudaEventRecord(s->ev[16], st));
-      KL(launch_slice_codes((int64_t)kept_pairs, s->klist, tlist, s->cams, s->aniso ? s->acams : nullptr,
-                            s->slice_lo, s->slice_hi, s->codes, st));
+      KL(launch_slice_codes((int64_t)nu, reinterpret_cast<const uint4*>(s->unit_meta), s->klist, s->cams,
+                            s->aniso ? s->acams : nullptr, s->slice_lo, s->slice_hi, s->codes, st));
       CK(cudaEventRecord(s->ev[17], st));
-      s->release(tlist);
-      KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile, nu, 1, st));
     }
     s->release(uc);
     s->release(uoff);
@@ -1637,7 +1637,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.codes = s->codes;
       va.aniso_fast = s->aniso_fast ? 1 : 0;
       int grid = 0;
-      KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, st, &grid));
+      KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, reinterpret_cast<const uint4*>(s->unit_meta),
+                          s->n_units, s->queue, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[10], st));
     CK(cudaMemcpyAsync(s->pin->vc, s->vcnt, sizeof(s->pin->vc), cudaMemcpyDeviceToHost, st));
@@ -2006,7 +2007,8 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   int g = 0;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)
-      return launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, s->n_units, s->queue, s->num_sms, s->stream, &g);
+      return launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, reinterpret_cast<const uint4*>(s->unit_meta),
+                              s->n_units, s->queue, s->num_sms, s->stream, &g);
     return launch_visibility_variant(variant - 1, va, s->num_sms, s->stream, &g);
   };
   KL(run());  // warm

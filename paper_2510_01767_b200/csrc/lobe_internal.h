@@ -141,7 +141,7 @@ cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float
 // per kept (tile, camera) pair (klist order): byte q = box_class of slice q
 // (0 reject, 2 accept, 1 | need << 2 undecided), so the test kernel loads
 // camera parameters only for undecided slices
-cudaError_t launch_slice_codes(int64_t n_kept, const uint32_t* klist, const uint32_t* tlist, const CamSetup* cams,
+cudaError_t launch_slice_codes(int64_t n_units, const uint4* unit_meta, const uint32_t* klist, const CamSetup* cams,
                                const AnisoCam* acams, const float4* slo, const float4* shi, uint32_t* codes,
                                cudaStream_t st);
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
@@ -149,9 +149,10 @@ cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_s
 // tile-major visibility over the kept lists: work units = (tile, <= kVisUnit cameras)
 constexpr int kVisUnit = 64;
 cudaError_t launch_units(const uint32_t* koff, int64_t n_tiles, int cmax, uint32_t* uc, const uint32_t* uoff,
-                         uint32_t* unit_tile, int64_t n_units, int phase, cudaStream_t st);
+                         uint32_t* unit_tile, uint4* unit_meta, int64_t n_units, int phase, cudaStream_t st);
 cudaError_t launch_vis_tiles(const VisArgs& a, const uint32_t* koff, const uint32_t* klist, const uint32_t* unit_tile,
-                             int64_t n_units, unsigned long long* queue, int num_sms, cudaStream_t st, int* grid_out);
+                             const uint4* unit_meta, int64_t n_units, unsigned long long* queue, int num_sms,
+                             cudaStream_t st, int* grid_out);
 // tuning variants of the same kernel (bit-identical outputs)
 int num_visibility_variants();
 cudaError_t launch_visibility_variant(int variant, const VisArgs& a, int num_sms, cudaStream_t st, int* grid_out);
