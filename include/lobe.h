@@ -18,7 +18,9 @@
  *     message valid until the next lobe_* call on the calling thread. After a
  *     failed call outputs are unspecified and the scene handle stays valid.
  *   - Ownership: the caller owns every pointer it passes. lobe_load_scene copies
- *     its inputs; the caller may free them on return. Outputs are caller-allocated
+ *     its inputs; the caller may free them on return (exception: the quaternion
+ *     arrays of a host-input load in the isotropic mode, see lobe_load_scene).
+ *     Outputs are caller-allocated
  *     with the sizes stated per call. The scene handle owns its device memory and
  *     is released by lobe_free_scene.
  *   - Pointers: output (and, with on_device, input) pointers may be host or
@@ -242,11 +244,18 @@ typedef struct {
  * (rows). Everything after this reuses the cached rows ("the back-projection
  * is computed once and reused"); the depth statistic (K_c, D_c,
  * z_min, z_max) is enqueued after the first crop kernel or by the first call
- * that needs it. Every input is validated before the call returns (host inputs
- * in the isotropic mode: the quaternions are copied last, on a side stream,
- * with their own check; the error names the first invalid Gaussian either
- * way). With a communicator this call is collective (NCCL communicators are
- * created here on first use). inout_frame may be NULL (= LOBE_FRAME_AUTO_ALL). */
+ * that needs it. Every input is validated, and the error names the first
+ * invalid Gaussian. Host inputs in the isotropic mode (the quaternions are only
+ * validated there): the positions are copied first (the spatial sort runs while
+ * the other fields travel), the quaternions last, on a side stream, with their
+ * own check, and this call returns without waiting for that check: its verdict
+ * (LOBE_E_INVALID_INPUT, naming the first invalid quaternion) is the status of
+ * the scene's next call, and of every call after it. The quaternion arrays of
+ * such a load are read after the call returns: keep them valid and unmodified
+ * until the scene's next call has returned (or lobe_free_scene). Every other
+ * input is consumed before the call returns. With a communicator this call is
+ * collective (NCCL communicators are created here on first use). inout_frame
+ * may be NULL (= LOBE_FRAME_AUTO_ALL). */
 lobe_status lobe_load_scene(const lobe_gaussians* gaussians, const lobe_camera* cameras, int64_t n_cams,
                             lobe_frame* inout_frame, const lobe_options* options, lobe_scene** out);
 void lobe_free_scene(lobe_scene* scene);

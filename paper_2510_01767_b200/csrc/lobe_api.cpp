@@ -132,7 +132,7 @@ struct DevBuf {
 
 }  // namespace
 
-constexpr int kNumEvents = 23;
+constexpr int kNumEvents = 25;
 
 struct lobe_scene {
   int device = 0;
@@ -255,8 +255,14 @@ struct lobe_scene {
   lobe_stats st{};
   cudaEvent_t ev[kNumEvents] = {};  // load pass: 0, 1, 8-12, 16, 17; evaluation: 2-4, 13; combine: 5, 6; dev bench:
                                     // 6, 7; crop: 14, 15; collective exchange: 18, 19; deferred quaternion
-                                    // check: 20 (done), 21 (k_prep_raw done), 22 (camera copies done)
+                                    // check: 20 (done), 21 (k_prep_raw done), 22 (camera copies done); split
+                                    // host-input copies: 23 (positions landed), 24 (other fields landed)
   cudaStream_t qstream = nullptr;   // host inputs, isotropic: quaternion copy + check (side stream)
+  // deferred quaternion verdict (event 20): pending after the load, then the
+  // status every later call reports (LOBE_E_INVALID_INPUT: the scene is unusable)
+  mutable bool q_pending = false;
+  mutable lobe_status q_status = LOBE_OK;
+  mutable unsigned long long q_first_bad = 0;
   // ---- communicator: collective calls, global outputs
   lobe::Comm* comm = nullptr;
   lobe::XOps* xops = nullptr;       // device-memory ops of comm on `stream`
@@ -538,8 +544,10 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   for (int zp = 0; zp < nzp; ++zp) s->zp_cell[zp] = (uint8_t)(Z.U.cell[zp / nzv] * g.n + Z.V.cell[zp % nzv]);
   s->pin->Z = Z;
   std::memcpy(s->pin->zp_cell, s->zp_cell.data(), nzp);
-  CK(cudaMemcpyAsync(s->dz, &s->pin->Z, sizeof(Z), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(s->d_zp_cell, s->pin->zp_cell, nzp, cudaMemcpyHostToDevice, st));
+  // (kernel uploads: a copy-engine transfer would queue behind the deferred
+  // quaternions of a host-input load)
+  KL(launch_upload(s->dz, &s->pin->Z, sizeof(Z), st));
+  KL(launch_upload(s->d_zp_cell, s->pin->zp_cell, nzp, st));
   CK(cudaMemsetAsync(s->zp_count, 0, sizeof(uint32_t) * kMaxZones * kMaxZones, st));
   // counts [3 x kMaxBlocks] u32 and incid [kMaxBlocks] u64 are one device block
   CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks, st));
@@ -1234,6 +1242,27 @@ lobe_status copy_out(lobe_scene* s, void* dst, const void* src, size_t bytes) {
 }  // namespace
 
 // ============================================================================
+// The deferred quaternion verdict of a host-input load (isotropic mode): known
+// once event 20 has completed. wait = false: report it only if already decided
+// (the call then refuses to run on an invalid scene); wait = true: decide now.
+static lobe_status scene_verdict(const lobe_scene* s, bool wait) {
+  if (!s) return LOBE_OK;
+  if (s->q_pending) {
+    if (!wait && cudaEventQuery(s->ev[20]) == cudaErrorNotReady) return LOBE_OK;
+    if (cudaEventSynchronize(s->ev[20]) != cudaSuccess) return fail(LOBE_E_CUDA, "quaternion check");
+    s->q_pending = false;
+    if (s->pin->q_err) {
+      s->q_status = LOBE_E_INVALID_INPUT;
+      s->q_first_bad = s->pin->q_bad;
+    }
+  }
+  if (s->q_status != LOBE_OK)
+    return fail(s->q_status, "gaussian " + std::to_string(s->q_first_bad) +
+                                 " invalid (|q| = 1 +- 1e-6, SPEC.md:30-33; reported after the load: the quaternions "
+                                 "of a host-input load are checked while the device works)");
+  return LOBE_OK;
+}
+
 extern "C" {
 
 const char* lobe_last_error(void) { return g_err.c_str(); }
@@ -1370,17 +1399,28 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     uint32_t* q_flags = nullptr;  // [0] err, [1..2] first bad index (u64)
     if (!g->on_device) {
       CK(s->alloc(&dev_in, (size_t)11 * G));
-      for (int k = 0; k < 11; ++k) {
-        din[k] = dev_in + (size_t)k * G;
-        if (q_defer && k >= 6 && k <= 9) continue;
-        CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
-      }
+      for (int k = 0; k < 11; ++k) din[k] = dev_in + (size_t)k * G;
       if (q_defer) {
+        // the copy engine is the bound of a host-input load (440 MB): positions
+        // first on the scene's stream, so the sort keys and the sort run while
+        // the scales and opacities follow on the side stream (strictly after
+        // the positions: event 23), then the camera tables, then the quaternions
         if (!s->qstream) s->qstream = acquire_side_stream(s->device);
         if (!s->qstream) return fail(LOBE_E_CUDA, "side stream creation failed");
+        for (int k = 0; k < 3; ++k)
+          CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(s->ev[23], st));
+        CK(cudaStreamWaitEvent(s->qstream, s->ev[23], 0));
+        for (int k : {3, 4, 5, 10})
+          CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice,
+                             s->qstream));
+        CK(cudaEventRecord(s->ev[24], s->qstream));
         CK(s->alloc(&q_flags, 4));
         const uint32_t qinit[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
         CK(cudaMemcpyAsync(q_flags, qinit, sizeof(qinit), cudaMemcpyHostToDevice, st));
+      } else {
+        for (int k = 0; k < 11; ++k)
+          CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
       }
     } else {
       for (int k = 0; k < 11; ++k) din[k] = src[k];
@@ -1393,7 +1433,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->d_cam_gv, NLc));
     if (s->aniso) CK(s->alloc(&s->acams, NLc));
     CK(s->alloc(&cr, (size_t)2 * NLc));
-    if (q_defer) CK(cudaEventRecord(s->ev[20], st));  // the side stream starts after the fields' copies
+    if (q_defer) CK(cudaEventRecord(s->ev[20], s->qstream));  // the camera copies follow the fields' copies
     // ---- a1 precompute
 
     float4* rec;
@@ -1423,17 +1463,25 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     pin.cov = cov_raw;
     pin.q_deferred = q_defer ? 1 : 0;
     tl.mark("inputs + a1 allocs");
+    // split host-input path: sort keys from the positions now, the records once
+    // the other fields have landed (after the sort, below)
+    pin.pass = q_defer ? 1 : 0;
     KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
     tl.mark("k_prep_raw launched");
-    // validation flags and the ground min / max reach the host asynchronously;
-    // they are checked at the first synchronisation (after the culling pass)
-    CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), cudaMemcpyDeviceToHost, st));
     size_t tmpb = 0;
     CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));  // top 24 of the 30-bit Morton keys
     void* tmp = nullptr;
     CK(malloc_async(&tmp, tmpb, st));
     CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st, 6, 30));
+    if (q_defer) {
+      CK(cudaStreamWaitEvent(st, s->ev[24], 0));
+      pin.pass = 2;
+      KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
+    }
+    // validation flags and the ground min / max reach the host asynchronously;
+    // they are checked at the first synchronisation (after the culling pass)
+    CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), cudaMemcpyDeviceToHost, st));
     CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->o2, (size_t)s->G_pad));
@@ -1715,14 +1763,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     CK(cudaEventRecord(s->ev[3], st));
     tl.mark("rest enqueued");
-    if (q_defer) {  // the deferred quaternion check decides before the load returns
-      CK(cudaEventSynchronize(s->ev[20]));
-      if (s->pin->q_err)
-        return fail(LOBE_E_INVALID_INPUT, "gaussian " + std::to_string(s->pin->q_bad) +
-                                              " invalid (finite, scale > 0, |q| = 1 +- 1e-6, opacity in [0,1]; "
-                                              "SPEC.md:30-33)");
-      tl.mark("quaternion check");
-    }
+    // the deferred quaternion check decides while the device works on: the
+    // load returns now if it is still running; every later scene call reports it
+    if (q_defer) s->q_pending = true;
     // no synchronisation here: the depth statistic may still run while the caller
     // enqueues the next call; event timings are read lazily (finalize_load_stats)
     s->kept_pairs_last = kept_pairs;
@@ -1747,7 +1790,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
   return LOBE_OK;
 }
 
-lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* K, double* depth_mean, float* z_min,
+static lobe_status impl_lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* K, double* depth_mean, float* z_min,
                                 float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member, int32_t* home) {
   LOBE_NVTX("lobe_assign_cameras");
   g_err.clear();
@@ -1804,7 +1847,7 @@ lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* 
   return LOBE_OK;
 }
 
-lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
+static lobe_status impl_lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
   LOBE_NVTX("lobe_block_loads");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
@@ -1827,7 +1870,7 @@ lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_lo
   return LOBE_OK;
 }
 
-lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
+static lobe_status impl_lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
   LOBE_NVTX("lobe_crop_masks");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
@@ -1843,7 +1886,7 @@ lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop
   return lobe_crop_from_masks(s, grid, s->masks, crop, eligible);
 }
 
-lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
+static lobe_status impl_lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
                                  uint64_t* eligible) {
   LOBE_NVTX("lobe_crop_from_masks");
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
@@ -1909,7 +1952,7 @@ lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uin
   return LOBE_OK;
 }
 
-lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
+static lobe_status impl_lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
                                uint64_t* incid) {
   LOBE_NVTX("lobe_block_partial");
   g_err.clear();
@@ -1926,7 +1969,7 @@ lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d
   return LOBE_OK;
 }
 
-lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
+static lobe_status impl_lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
                                uint32_t* g_vis) {
   LOBE_NVTX("lobe_masks_combine");
   g_err.clear();
@@ -1943,7 +1986,7 @@ lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathe
   return LOBE_OK;
 }
 
-lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint32_t* n_cams, const uint64_t* incid,
+static lobe_status impl_lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint32_t* n_cams, const uint64_t* incid,
                                const uint32_t* g_vis, lobe_block_load* out, uint32_t* objective) {
   LOBE_NVTX("lobe_block_records");
   g_err.clear();
@@ -1955,7 +1998,7 @@ lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint3
   return LOBE_OK;
 }
 
-lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t* rows) {
+static lobe_status impl_lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t* rows) {
   LOBE_NVTX("lobe_export_rows");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
@@ -1972,7 +2015,7 @@ lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t*
   return LOBE_OK;
 }
 
-lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
+static lobe_status impl_lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
   LOBE_NVTX("lobe_dev_vis_bench");
   // variant 0: tile-major kernel over the kept lists (production);
   // 1-5: the camera-inner kernel (1 = culled, 2 = dense: every test evaluated)
@@ -2021,7 +2064,7 @@ lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, flo
   return LOBE_OK;
 }
 
-lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
+static lobe_status impl_lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
                                 lobe_subscene* out, int64_t capacity) {
   LOBE_NVTX("lobe_block_subscene");
   g_err.clear();
@@ -2078,7 +2121,7 @@ lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t bl
   return rs;
 }
 
-lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+static lobe_status impl_lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
                               const float* grad, const float* normals, float tau_grad, float scale_split,
                               lobe_subscene* out, int64_t capacity) {
   LOBE_NVTX("lobe_densify_step");
@@ -2113,7 +2156,7 @@ lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t bloc
   return rs;
 }
 
-lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+static lobe_status impl_lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
                                lobe_subscene* out, int64_t capacity) {
   LOBE_NVTX("lobe_prune_outside");
   g_err.clear();
@@ -2144,7 +2187,7 @@ lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t blo
   return rs;
 }
 
-lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
+static lobe_status impl_lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
                               int64_t capacity) {
   LOBE_NVTX("lobe_merge_blocks");
   g_err.clear();
@@ -2249,7 +2292,7 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
   return LOBE_OK;
 }
 
-lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
+static lobe_status impl_lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
                                float eps_w) {
   LOBE_NVTX("lobe_render_select");
   g_err.clear();
@@ -2295,7 +2338,7 @@ lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int3
   return LOBE_OK;
 }
 
-lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity) {
+static lobe_status impl_lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity) {
   LOBE_NVTX("lobe_camera_clouds");
   g_err.clear();
   if (!s) return fail(LOBE_E_STATE, "scene is NULL");
@@ -2316,7 +2359,7 @@ lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float
   return LOBE_OK;
 }
 
-lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
+static lobe_status impl_lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
                              float* depth, float* weight) {
   LOBE_NVTX("lobe_render_maps");
   g_err.clear();
@@ -2344,7 +2387,7 @@ lobe_status lobe_scene_info(const lobe_scene* s, int64_t* n_gaussians, int64_t* 
   return LOBE_OK;
 }
 
-lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
+static lobe_status impl_lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
   LOBE_NVTX("lobe_get_stats");
   if (!s || !out) return fail(LOBE_E_STATE, "NULL");
   finalize_load_stats(const_cast<lobe_scene*>(s));
@@ -2376,7 +2419,7 @@ lobe_status lobe_bo_run(int32_t m, int32_t n, const lobe_balance_opts* opts, lob
   return LOBE_OK;
 }
 
-lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lobe_balance_opts* opts, float* v_out,
+static lobe_status impl_lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lobe_balance_opts* opts, float* v_out,
                                    float* h_out, uint32_t* history, float* cut_history, lobe_block_load* best) {
   LOBE_NVTX("lobe_balance_partition");
   g_err.clear();
@@ -2419,6 +2462,132 @@ lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lo
     TRY(lobe_block_loads(s, &gr, best, &obj));
   }
   return LOBE_OK;
+}
+
+
+// ---- exported scene calls: a host-input load in the isotropic mode returns
+// before the deferred quaternion check has decided (the copy engine is the
+// bound of that load and the quaternions travel last); every scene call reports
+// its verdict: before its work if already known, else before it returns.
+lobe_status lobe_assign_cameras(lobe_scene* s, const lobe_grid* grid, uint32_t* K, double* depth_mean, float* z_min,
+                                float* z_max, uint32_t* n_cb, uint32_t* n0_cb, uint64_t* member, int32_t* home) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_assign_cameras(s, grid, K, depth_mean, z_min, z_max, n_cb, n0_cb, member, home);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_block_loads(lobe_scene* s, const lobe_grid* grid, lobe_block_load* out, uint32_t* objective) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_block_loads(s, grid, out, objective);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_crop_masks(lobe_scene* s, const lobe_grid* grid, uint64_t* crop, uint64_t* eligible) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_crop_masks(s, grid, crop, eligible);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_crop_from_masks(lobe_scene* s, const lobe_grid* grid, const uint32_t* d_masks, uint64_t* crop,
+                                 uint64_t* eligible) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_crop_from_masks(s, grid, d_masks, crop, eligible);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_block_partial(lobe_scene* s, const lobe_grid* grid, uint32_t* d_masks, uint32_t* n_cams,
+                               uint64_t* incid) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_block_partial(s, grid, d_masks, n_cams, incid);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_masks_combine(lobe_scene* s, int32_t B, const uint32_t* d_gathered, int32_t W, uint32_t* d_out,
+                               uint32_t* g_vis) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_masks_combine(s, B, d_gathered, W, d_out, g_vis);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_block_records(lobe_scene* s, const lobe_grid* grid, const uint32_t* n_cams, const uint64_t* incid,
+                               const uint32_t* g_vis, lobe_block_load* out, uint32_t* objective) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_block_records(s, grid, n_cams, incid, g_vis, out, objective);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_export_rows(lobe_scene* s, int64_t c0, int64_t count, uint32_t* rows) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_export_rows(s, c0, count, rows);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32_t reps, float* ms, int32_t* grid) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_dev_vis_bench(s, variant, reps, ms, grid);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_block_subscene(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_gaussians* coarse,
+                                lobe_subscene* out, int64_t capacity) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_block_subscene(s, grid, block, coarse, out, capacity);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_densify_step(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                              const float* grad, const float* normals, float tau_grad, float scale_split,
+                              lobe_subscene* out, int64_t capacity) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_densify_step(s, grid, block, in, grad, normals, tau_grad, scale_split, out, capacity);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_prune_outside(lobe_scene* s, const lobe_grid* grid, int32_t block, const lobe_subscene* in,
+                               lobe_subscene* out, int64_t capacity) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_prune_outside(s, grid, block, in, out, capacity);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_merge_blocks(lobe_scene* s, const lobe_subscene* subs, int32_t count, lobe_subscene* out,
+                              int64_t capacity) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_merge_blocks(s, subs, count, out, capacity);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_render_select(lobe_scene* s, const lobe_gaussians* coarse, int32_t downscale, int32_t stride,
+                               float eps_w) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_render_select(s, coarse, downscale, stride, eps_w);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_camera_clouds(lobe_scene* s, int64_t* offsets, float* gu, float* gv, int64_t capacity) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_camera_clouds(s, offsets, gu, gv, capacity);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_render_maps(lobe_scene* s, const lobe_gaussians* coarse, int64_t camera, int32_t downscale,
+                             float* depth, float* weight) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_render_maps(s, coarse, camera, downscale, depth, weight);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_get_stats(const lobe_scene* s, lobe_stats* out) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_get_stats(s, out);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
+}
+
+lobe_status lobe_balance_partition(lobe_scene* s, int32_t m, int32_t n, const lobe_balance_opts* opts, float* v_out,
+                                   float* h_out, uint32_t* history, float* cut_history, lobe_block_load* best) {
+  TRY(scene_verdict(s, false));
+  const lobe_status r = impl_lobe_balance_partition(s, m, n, opts, v_out, h_out, history, cut_history, best);
+  return r != LOBE_OK ? r : scene_verdict(s, true);
 }
 
 }  // extern "C"

@@ -59,6 +59,11 @@ struct PrepIn {
   float c0[3], rho, au[3], av[3];
   float* cov;  // anisotropic predicate: 6 floats per Gaussian (caller order), else NULL
   int q_deferred;  // 1: the quaternions are validated by k_check_quats (host inputs, isotropic)
+  // 0: one pass over every field; split passes for host inputs (the positions
+  // arrive first, so the sort runs while the other fields are still in flight):
+  // 1: positions only -> sort keys / values, ground min / max, position checks;
+  // 2: the records (every field; keys, values and the min / max untouched)
+  int pass;
 };
 // |q| = 1 +- 1e-6, the check k_prep_raw applies, for the deferred
 // path: err |= 1 and err_idx = min index of an invalid quaternion
@@ -162,6 +167,8 @@ cudaError_t launch_depth_pairs(int64_t n_tiles, const uint32_t* tile_off, const 
                                const float2* o2, const CamSetup* cams, PairPartial* out, int ctas_per_sm,
                                unsigned long long* tile_queue, cudaStream_t st);
 cudaError_t launch_cam_counts(int64_t n_pairs, const uint32_t* pair_cam, uint32_t* counts, cudaStream_t st);
+// copy from pinned (mapped) host memory by a kernel, not the copy engine
+cudaError_t launch_upload(void* dst, const void* src_pinned, size_t bytes, cudaStream_t st);
 cudaError_t launch_iota(int32_t* v, int64_t n, cudaStream_t st);
 cudaError_t launch_depth_reduce(int64_t n_cams, const uint32_t* cam_off, const int32_t* order, const PairPartial* part,
                                 uint32_t* K, double* D, float* zmin, float* zmax, cudaStream_t st);
