@@ -260,6 +260,13 @@ struct lobe_scene {
   cudaStream_t qstream = nullptr;   // host inputs, isotropic: quaternion copy + check (side stream)
   // deferred quaternion verdict (event 20): pending after the load, then the
   // status every later call reports (LOBE_E_INVALID_INPUT: the scene is unusable)
+  // render-selection scratch (lobe_render_select): grow-only device blocks kept
+  // for the scene's lifetime, so repeated selections neither allocate nor free
+  struct RBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  RBuf rscratch[20];
   mutable bool q_pending = false;
   mutable lobe_status q_status = LOBE_OK;
   mutable unsigned long long q_first_bad = 0;
@@ -780,19 +787,13 @@ struct RenderJob {
   // k_render roofline: (pixel, splat) tests / composited (device counters), kernel time
   unsigned long long* counters = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;  // around each batch's k_render
-  // grow-only scratch reused by every batch (no pool growth between batches)
-  struct Buf {
-    void* p = nullptr;
-    size_t cap = 0;
-  };
-  Buf b[20];
 };
 
 // device scratch slot `k` of at least `bytes` bytes (grow-only)
 template <class T>
 lobe_status scratch(lobe_scene* s, RenderJob& J, int k, T** out, size_t count) {
   const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
-  RenderJob::Buf& b = J.b[k];
+  lobe_scene::RBuf& b = s->rscratch[k];
   if (b.cap < bytes) {
     // 1.5x headroom: later batches rarely need a new block. Plain cudaMalloc:
     // growing the stream-ordered pool by these multi-GB blocks is far slower
@@ -810,19 +811,9 @@ lobe_status scratch(lobe_scene* s, RenderJob& J, int k, T** out, size_t count) {
   *out = static_cast<T*>(b.p);
   return LOBE_OK;
 }
-void free_scratch(lobe_scene* s, RenderJob& J) {
-  cudaStreamSynchronize(s->stream);
-  for (auto& b : J.b)
-    if (b.p) {
-      cudaFree(b.p);
-      b.p = nullptr;
-      b.cap = 0;
-    }
-}
-
 lobe_status grow_cloud(lobe_scene* s, RenderJob& J, int64_t need) {
   if (need <= J.cap) return LOBE_OK;
-  const int64_t cap = std::max<int64_t>(need, J.cap * 2);
+  const int64_t cap = std::max<int64_t>({need, J.cap * 2, 1});
   float *gu = nullptr, *gv = nullptr;
   uint32_t* cam = nullptr;
   CK(s->alloc(&gu, (size_t)cap));
@@ -1277,6 +1268,15 @@ void lobe_free_scene(lobe_scene* s) {
   if (!s) return;
   cudaSetDevice(s->device);
   if (s->a4_side && !s->a4_joined) cudaStreamWaitEvent(s->stream, s->ev[12], 0);  // a4 reads what is freed below
+  bool synced = false;
+  for (auto& b : s->rscratch)  // render-selection scratch (plain cudaMalloc blocks)
+    if (b.p) {
+      if (!synced) cudaStreamSynchronize(s->stream);
+      synced = true;
+      cudaFree(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+    }
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
   s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
@@ -2257,14 +2257,59 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
   CK(cudaMemcpyAsync(hK.data(), s->K, sizeof(uint32_t) * std::max<int64_t>(NL, 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   std::vector<lobe_camera> hcams(s->host_cams.begin(), s->host_cams.end());
+  {  // the clouds at their upper bound (one point per sample pixel) in one block:
+     // growing them batch by batch re-copied them and grew the pool (~0.5 s)
+    int64_t bound = J.n;
+    for (int64_t c = cb; c < ce; ++c) {
+      const int64_t wd = hcams[c].width / J.ds, hd = hcams[c].height / J.ds;
+      bound += ((wd + J.stride - 1) / J.stride) * ((hd + J.stride - 1) / J.stride);
+    }
+    TRY(grow_cloud(s, J, bound));
+  }
   // batches bounded by the records they hold (the splats of their visible Gaussians)
   const uint64_t kBudget = 48ull << 20;
+  auto batch_end = [&](int64_t c, uint64_t* recs) {
+    int64_t e = c;
+    *recs = 0;
+    while (e < ce && (e == c || *recs + hK[e] <= kBudget) && e - c < 2048) *recs += hK[e++];
+    return e;
+  };
+  {  // the scratch blocks at the largest batch's sizes before the first batch
+     // (records = sum of K_c exactly; tile entries still grow on demand)
+    uint64_t mrec = 1, mpairs = 1, mcam = 1, mtiles = 1, mmaps = 1, msamp = 1;
+    for (int64_t c = cb; c < ce;) {
+      uint64_t recs = 0;
+      const int64_t e = batch_end(c, &recs);
+      uint64_t tiles = 0, maps = 0, samp = 0;
+      for (int64_t q = c; q < e; ++q) {
+        const int64_t wd = hcams[q].width / J.ds, hd = hcams[q].height / J.ds;
+        tiles += (uint64_t)(((wd + 15) / 16) * ((hd + 15) / 16));
+        maps += (uint64_t)(wd * hd);
+        samp += (uint64_t)(((wd + J.stride - 1) / J.stride) * ((hd + J.stride - 1) / J.stride));
+      }
+      mrec = std::max<uint64_t>(mrec, recs);
+      mpairs = std::max<uint64_t>(mpairs, (uint64_t)hoff[e] - hoff[c]);
+      mcam = std::max<uint64_t>(mcam, (uint64_t)(e - c));
+      mtiles = std::max(mtiles, tiles);
+      mmaps = std::max(mmaps, maps);
+      msamp = std::max(msamp, samp);
+      c = e;
+    }
+    uint8_t* d = nullptr;
+    const uint64_t s12 = std::max(std::max(mpairs, mrec), msamp) + 1;
+    const std::pair<int, uint64_t> want[] = {
+        {0, sizeof(RenderCam) * mcam}, {1, 4 * s12},       {2, 4 * s12},          {3, 8 * mrec},
+        {4, 8 * mrec},                 {5, 4 * mrec},      {6, 4 * mrec},         {7, 4 * mrec},
+        {8, 40 * mrec},                {9, 4 * (mcam + 1)}, {11, 4 * (msamp + 1)}, {12, 4 * (msamp + 1)},
+        {15, 4 * (mtiles + 1)},        {16, 4 * (mtiles + 1)}, {17, 4 * mmaps},    {18, 4 * mmaps},
+        {19, 4 * (mcam + 1)}};
+    for (const auto& w : want) TRY(scratch(s, J, w.first, &d, (size_t)w.second));
+  }
   const bool trace = std::getenv("LOBE_TRACE") != nullptr;
   int64_t c = cb;
   while (c < ce) {
-    int64_t e = c;
     uint64_t recs = 0;
-    while (e < ce && (e == c || recs + hK[e] <= kBudget) && e - c < 2048) recs += hK[e++];
+    const int64_t e = batch_end(c, &recs);
     const auto t0 = std::chrono::steady_clock::now();
     TRY(render_batch(s, prec, hoff, hcams, c, e, J));
     if (trace) {
@@ -2276,7 +2321,6 @@ lobe_status render_cameras(lobe_scene* s, const lobe_gaussians* coarse, int64_t 
     c = e;
   }
   s->release(prec);
-  free_scratch(s, J);
   if (cloud_counts) {
     // cloud size per local camera (integer atomics: order-free)
     cloud_counts->assign(std::max<int64_t>(NL, 1), 0);
