@@ -147,6 +147,7 @@ struct lobe_scene {
   float *xy = nullptr, *zk = nullptr, *o2 = nullptr, *gu = nullptr, *gv = nullptr;
   int32_t* iperm = nullptr;
   CamSetup* cams = nullptr;
+  CamSetup* cam_pat = nullptr;  // [N_loc x kPatterns] pattern-ordered copies (k_vis_tiles)
   float *d_cam_gu = nullptr, *d_cam_gv = nullptr;
   uint32_t* rows = nullptr;
   uint8_t* flags = nullptr;     // dev bench (camera-inner variants) only
@@ -1278,7 +1279,7 @@ void lobe_free_scene(lobe_scene* s) {
       b.cap = 0;
     }
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
-  s->release(s->iperm); s->release(s->cams); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
+  s->release(s->iperm); s->release(s->cams); s->release(s->cam_pat); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
   s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->unit_meta); s->release(s->queue); s->release(s->K); s->release(s->D);
@@ -1429,6 +1430,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     const int64_t NLc = std::max<int64_t>(s->N_loc, 1);
     float* cr = nullptr;  // camera-centre raw grid coordinates
     CK(s->alloc(&s->cams, NLc));
+    CK(s->alloc(&s->cam_pat, (size_t)NLc * kPatterns));
     CK(s->alloc(&s->d_cam_gu, NLc));
     CK(s->alloc(&s->d_cam_gv, NLc));
     if (s->aniso) CK(s->alloc(&s->acams, NLc));
@@ -1654,6 +1656,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       KL(launch_units(s->koff, s->n_tiles, kVisUnit, nullptr, uoff, s->unit_tile,
                        reinterpret_cast<uint4*>(s->unit_meta), nu, 1, st));
       CK(cudaEventRecord(s->ev[16], st));
+      if (!s->aniso) KL(launch_cam_patterns(s->cams, s->N_loc, s->cam_pat, st));
       KL(launch_slice_codes((int64_t)nu, reinterpret_cast<const uint4*>(s->unit_meta), s->klist, s->cams,
                             s->aniso ? s->acams : nullptr, s->slice_lo, s->slice_hi, s->codes, st));
       CK(cudaEventRecord(s->ev[17], st));
@@ -1684,6 +1687,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.acams = s->acams;
       va.codes = s->codes;
       va.aniso_fast = s->aniso_fast ? 1 : 0;
+      va.cam_pat = s->cam_pat;
       int grid = 0;
       KL(launch_vis_tiles(va, s->koff, s->klist, s->unit_tile, reinterpret_cast<const uint4*>(s->unit_meta),
                           s->n_units, s->queue, s->num_sms, st, &grid));
@@ -2046,6 +2050,7 @@ static lobe_status impl_lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32
   va.acams = s->acams;
   va.codes = s->codes;
   va.aniso_fast = s->aniso_fast ? 1 : 0;
+  va.cam_pat = s->cam_pat;
   if (s->aniso && variant != 0) return fail(LOBE_E_INVALID_CONFIG, "camera-inner variants are isotropic only");
   int g = 0;
   auto run = [&]() -> cudaError_t {

@@ -128,6 +128,8 @@ struct VisArgs {
   const AnisoCam* acams;         // anisotropic: per local camera
   const uint32_t* codes;         // k_vis_tiles (isotropic): per kept pair, the 4 slices' box_class codes (8 bits each)
   int aniso_fast;                // anisotropic: every camera's depth range within [2^-126, 2^126] (branch-free rcp/sqrt)
+  const CamSetup* cam_pat;       // k_vis_tiles (isotropic): per local camera, kPatterns copies of its
+                                 // CamSetup with the fields in each open-condition pattern's test order
 };
 
 // Tile culling: per camera the five linear forms of the
@@ -146,6 +148,10 @@ cudaError_t launch_cull(const float4* tlo, const float4* thi, float4* clo, float
 // per kept (tile, camera) pair (klist order): byte q = box_class of slice q
 // (0 reject, 2 accept, 1 | need << 2 undecided), so the test kernel loads
 // camera parameters only for undecided slices
+// kPatterns pattern-ordered copies of every camera's CamSetup (k_vis_tiles stages
+// the copy of a slice's open-condition pattern as is)
+constexpr int kPatterns = 9;
+cudaError_t launch_cam_patterns(const CamSetup* cams, int64_t n_cams, CamSetup* cam_pat, cudaStream_t st);
 cudaError_t launch_slice_codes(int64_t n_units, const uint4* unit_meta, const uint32_t* klist, const CamSetup* cams,
                                const AnisoCam* acams, const float4* slo, const float4* shi, uint32_t* codes,
                                cudaStream_t st);
