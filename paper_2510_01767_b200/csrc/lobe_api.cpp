@@ -194,6 +194,7 @@ struct lobe_scene {
   int64_t n_pairs = 0;
   // evaluation scratch
   uint16_t *zp = nullptr, *word_zone = nullptr, *tile_zone = nullptr;
+  uint4* wbox = nullptr;  // per row word: gu / gv range of its Gaussians (a5)
   uint32_t* zp_count = nullptr;
   ZoneTables* dz = nullptr;
   uint8_t* d_zp_cell = nullptr;
@@ -560,7 +561,8 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
   // counts [3 x kMaxBlocks] u32 and incid [kMaxBlocks] u64 are one device block
   CK(cudaMemsetAsync(s->counts, 0, sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks, st));
   CK(cudaEventRecord(s->ev[2], st));
-  KL(launch_zones(s->dz, nzv, nzp, s->G, s->G_pad, s->gu, s->gv, s->zp, s->word_zone, s->tile_zone, s->zp_count, st));
+  KL(launch_zones(s->dz, nzv, nzp, s->G, s->G_pad, s->gu, s->gv, s->wbox, s->zp, s->word_zone, s->tile_zone,
+                  s->zp_count, st));
   KL(launch_gblk(s->dz, nzv, nzp, s->zp_count, s->counts + 2 * kMaxBlocks, st));
   // ---- a6 histograms
   TRY(ensure_hist_cap(s, (size_t)std::max<int64_t>(s->N_loc, 1) * nzp));
@@ -1278,7 +1280,7 @@ void lobe_free_scene(lobe_scene* s) {
       b.p = nullptr;
       b.cap = 0;
     }
-  s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv);
+  s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv); s->release(s->wbox);
   s->release(s->iperm); s->release(s->cams); s->release(s->cam_pat); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
   s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
@@ -1489,9 +1491,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->o2, (size_t)s->G_pad));
     CK(s->alloc(&s->gu, (size_t)s->G_pad));
     CK(s->alloc(&s->gv, (size_t)s->G_pad));
+    CK(s->alloc(&s->wbox, (size_t)s->G_pad / 32));
     CK(s->alloc(&s->iperm, (size_t)G));
     if (s->aniso) CK(s->alloc(&s->cv, (size_t)s->G_pad / 2 * 3));
-    KLN(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, st), 2);
+    KLN(launch_pack(G, s->G_pad, perm, rec, scratch + 1, s->xy, s->zk, s->o2, s->gu, s->gv, s->iperm, cov_raw, s->cv, s->wbox, st), 2);
     tl.mark("sort + k_pack launched");
     s->release(cov_raw);
     cudaFreeAsync(tmp, st);
@@ -1933,7 +1936,7 @@ static lobe_status impl_lobe_crop_from_masks(lobe_scene* s, const lobe_grid* gri
   CK(s->alloc(&mbits, (size_t)s->words * 32));
   CK(s->alloc(&cb8, (size_t)s->words * 32));
   CK(cudaEventRecord(s->ev[14], s->stream));
-  KLN(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream), 2);
+  KLN(launch_crop(s->G, s->iperm, s->zp, s->word_zone, s->d_zp_cell, d_masks, s->words, g.B, mbits, cb8, dc, de, s->stream), 2);
   CK(cudaEventRecord(s->ev[15], s->stream));
   // a pending a4 (depth statistic) goes on the scene's stream now, so it runs
   // while the masks travel to the host on the side stream (copy engines)
@@ -2093,7 +2096,7 @@ static lobe_status impl_lobe_block_subscene(lobe_scene* s, const lobe_grid* grid
     uint8_t* cb8 = nullptr;
     CK(s->alloc(&mbits, (size_t)s->words * 32));
     CK(s->alloc(&cb8, (size_t)s->words * 32));
-    KLN(launch_crop(s->G, s->iperm, s->zp, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
+    KLN(launch_crop(s->G, s->iperm, s->zp, s->word_zone, s->d_zp_cell, s->masks, s->words, g.B, mbits, cb8,
                    reinterpret_cast<uint32_t*>(dc), reinterpret_cast<uint32_t*>(de), st), 2);
     s->release(mbits);
     s->release(cb8);

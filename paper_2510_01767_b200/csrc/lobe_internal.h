@@ -96,9 +96,12 @@ cudaError_t radix_sort_pairs(void* tmp, size_t& tmp_bytes, const uint32_t* kin, 
 // Gather into the internal pair-interleaved layout, build the inverse permutation;
 // anisotropic: also Sigma, cv[3 (32 g + l) + {0,1,2}] = {S00A,S00B,S01A,S01B},
 // {S02A,S02B,S11A,S11B}, {S12A,S12B,S22A,S22B}.
+// wbox (may be NULL): per 32-Gaussian row word, the {min, max} of its real
+// Gaussians' gu and gv as float bits {umin, umax, vmin, vmax} (a padding-only
+// word: {~0, 0, ~0, 0}); a5 resolves zone-uniform words from it
 cudaError_t launch_pack(int64_t G, int64_t G_pad, const int32_t* perm, const float4* rec, const uint32_t* mm_ord,
                         float* xy, float* zk, float* o2, float* gu, float* gv, int32_t* iperm, const float* cov_raw,
-                        float4* cv, cudaStream_t st);
+                        float4* cv, uint4* wbox, cudaStream_t st);
 
 // a3: visibility tests -> rows, tile flags, per-(chunk,camera) partials.
 struct VisArgs {
@@ -193,9 +196,11 @@ cudaError_t launch_cam_scatter(const uint32_t* tile_off, int64_t n_tiles, int64_
                                int64_t tw, const uint32_t* cam_off, int32_t* cam_order, cudaStream_t st);
 
 // a5: per-Gaussian zone pair, per-word / per-tile uniform zone, per-zone counts.
+// zp is written only for the words whose box straddles a zone boundary (the
+// others are resolved from their word box: word_zone != kMixed there)
 cudaError_t launch_zones(const ZoneTables* dz, int nzv, int nzp, int64_t G, int64_t G_pad, const float* gu,
-                         const float* gv, uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone, uint32_t* zp_count,
-                         cudaStream_t st);
+                         const float* gv, const uint4* wbox, uint16_t* zp, uint16_t* word_zone, uint16_t* tile_zone,
+                         uint32_t* zp_count, cudaStream_t st);
 // a6: zone-pair histograms per camera from the (tile, camera) pairs.
 // a6 per (tile, batch of 32 cameras of the tile's non-empty list)
 cudaError_t launch_hist(int64_t n_tiles, const uint32_t* tile_off, const uint32_t* pair_cam, const uint32_t* rows,
@@ -232,7 +237,8 @@ cudaError_t launch_xcounts(const uint32_t* ncams, const unsigned long long* inci
 // a9: caller-order crop / eligible masks.
 // mt: scratch, B x words u32 (word-major transpose of masks)
 // a9: per-Gaussian block bits (scratch mbits, cb8: words * 32 entries each), then the caller-order gather
-cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint8_t* zp_cellblock,
+cudaError_t launch_crop(int64_t G, const int32_t* iperm, const uint16_t* zp, const uint16_t* word_zone,
+                        const uint8_t* zp_cellblock,
                         const uint32_t* masks, int64_t words, int B, uint64_t* mbits, uint8_t* cb8, uint32_t* crop32,
                         uint32_t* elig32, cudaStream_t st);
 cudaError_t launch_export_rows(int64_t G, const int32_t* iperm, const uint32_t* rows, int64_t words, int64_t c0,
