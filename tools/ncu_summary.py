@@ -26,6 +26,7 @@ METRICS = {
     "registers_per_thread": ("launch__registers_per_thread", 1.0),
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+TIME_TO_MS = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}
 
 
 def main():
@@ -48,6 +49,8 @@ def main():
             val = float(v[i].replace(",", ""))
             if key.startswith("dram_"):
                 val *= SCALE.get(units[i], 1)
+            if key == "duration_ms":  # ncu picks the unit per report
+                val *= TIME_TO_MS.get(units[i], 1.0)
             out[key] = val
     if "dram_read_bytes" in out and "dram_write_bytes" in out:
         out["dram_bytes_per_launch"] = out["dram_read_bytes"] + out["dram_write_bytes"]
