@@ -1005,13 +1005,24 @@ static int a4_side_ctas() {
   return v;
 }
 
-lobe_status launch_a4(lobe_scene* s, cudaStream_t st) {
+// ... and when it runs alone on the scene's stream (deferred): one resident
+// wave over the tile queue at full occupancy (LOBE_A4_CTAS_ALONE overrides;
+// 0 = two waves, grid-stride)
+static int a4_alone_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("LOBE_A4_CTAS_ALONE");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+
+lobe_status launch_a4(lobe_scene* s, cudaStream_t st, bool side) {
   const int64_t NL = std::max<int64_t>(s->N_loc, 1), cap = s->a4_cap, tw = s->a4_tw;
   if (s->N_loc > 0) {
     KL(launch_depth_pairs(s->n_tiles, s->tile_off, s->pair_cam, s->rows, s->words,
                           reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk),
                           reinterpret_cast<const float2*>(s->o2), s->cams, s->pair_part,
-                          st == s->dstream ? a4_side_ctas() : 0, s->queue + 1, st));
+                          side ? a4_side_ctas() : a4_alone_ctas(), s->queue + 1, st));
     // pair indices in camera-major order, tile order within a camera
     uint32_t *ccount = nullptr, *wordpre = nullptr;
     CK(malloc_async(&ccount, sizeof(uint32_t) * ((size_t)NL + 1), st));
@@ -1044,7 +1055,7 @@ lobe_status ensure_a4(lobe_scene* s, bool join = true) {
   if (s->a4_pending) {
     s->a4_pending = false;
     CK(cudaEventRecord(s->ev[11], s->stream));
-    return launch_a4(s, s->stream);
+    return launch_a4(s, s->stream, false);
   }
   if (s->a4_side && join && !s->a4_joined) {
     CK(cudaStreamWaitEvent(s->stream, s->ev[12], 0));
@@ -1747,7 +1758,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       if (!s->dstream) return fail(LOBE_E_CUDA, "side stream creation failed");
       CK(cudaEventRecord(s->ev[11], st));
       CK(cudaStreamWaitEvent(s->dstream, s->ev[11], 0));
-      TRY(launch_a4(s, s->dstream));
+      TRY(launch_a4(s, s->dstream, true));
       s->a4_side = true;
       s->a4_joined = false;
     } else {
