@@ -165,6 +165,8 @@ struct lobe_scene {
   float4 *tile_lo = nullptr, *tile_hi = nullptr, *chunk_lo = nullptr, *chunk_hi = nullptr;
   float4 *slice_lo = nullptr, *slice_hi = nullptr;
   uint32_t* codes = nullptr;  // per kept pair: slice classes (k_slice_codes)
+  float4 *group_lo = nullptr, *group_hi = nullptr;  // anisotropic: 64-Gaussian pair-group boxes
+  uint32_t* gcodes = nullptr;  // anisotropic: per kept pair, pair-group classes of undecided slices
   bool aniso_fast = true;     // anisotropic test may use the branch-free rcp / sqrt (all depth ranges in range)
   cudaStream_t side = nullptr;  // per-camera host copies (run_staged), created on first use
   bool aniso = false;            // anisotropic predicate (ledger L24)
@@ -1079,8 +1081,10 @@ void finalize_load_stats(lobe_scene* s) {
   s->n_pairs = s->pin->n_pairs;
   s->st.tile_pairs = (uint64_t)s->n_pairs;
   s->st.kept_tests = (uint64_t)s->kept_pairs_last * (uint64_t)kTile;  // pairs surviving the tile bound
-  s->st.dense_tests = (uint64_t)s->pin->vc[0] * (uint64_t)(kTile / 4);  // exact tests run (undecided slices)
-  s->st.accepted_tests = (uint64_t)s->pin->vc[1] * (uint64_t)(kTile / 4);
+  // exact tests run, counted by the test kernels (real Gaussians of the undecided
+  // slices, less the anisotropic pair groups their own box decided)
+  s->st.dense_tests = (uint64_t)s->pin->vc[11];
+  s->st.accepted_tests = (uint64_t)s->pin->vc[10];  // slices and (anisotropic) pair groups accepted
   for (int p = 0; p < 9; ++p) s->st.exact_pattern_tests[p] = (uint64_t)s->pin->vc[16 + p] * (uint64_t)(kTile / 4);
   for (int v = 0; v < 4; ++v) s->st.exact_variant_tests[v] = s->st.exact_pattern_tests[v];
   s->st.exact_variant_tests[4] = s->st.exact_pattern_tests[4] + s->st.exact_pattern_tests[5] +
@@ -1294,7 +1298,7 @@ void lobe_free_scene(lobe_scene* s) {
   s->release(s->xy); s->release(s->zk); s->release(s->o2); s->release(s->gu); s->release(s->gv); s->release(s->wbox);
   s->release(s->iperm); s->release(s->cams); s->release(s->cam_pat); s->release(s->d_cam_gu); s->release(s->d_cam_gv);
   s->release(s->rows); s->release(s->flags); s->release(s->nonempty); s->release(s->pair_part); s->release(s->cam_off); s->release(s->cam_order);
-  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
+  s->release(s->tile_lo); s->release(s->tile_hi); s->release(s->chunk_lo); s->release(s->chunk_hi); s->release(s->cv); s->release(s->acams); s->release(s->cloud_gu); s->release(s->cloud_gv); s->release(s->cloud_cam); s->release(s->cloud_K); s->release(s->slice_lo); s->release(s->slice_hi); s->release(s->codes); s->release(s->group_lo); s->release(s->group_hi); s->release(s->gcodes); s->release(s->vcnt); s->release(s->keep); s->release(s->kept);
   s->release(s->koff); s->release(s->klist); s->release(s->unit_tile); s->release(s->unit_meta); s->release(s->queue); s->release(s->K); s->release(s->D);
   s->release(s->zmin); s->release(s->zmax); s->release(s->tile_off); s->release(s->pair_cam);
   s->release(s->pair_tile); s->release(s->zp); s->release(s->word_zone); s->release(s->tile_zone);
@@ -1582,8 +1586,12 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->chunk_hi, (size_t)s->n_chunks));
     CK(s->alloc(&s->keep, (size_t)s->n_tiles * s->n_sub));
     CK(s->alloc(&s->kept, 1));
+    if (s->aniso) {
+      CK(s->alloc(&s->group_lo, (size_t)s->n_tiles * 16));
+      CK(s->alloc(&s->group_hi, (size_t)s->n_tiles * 16));
+    }
     KL(launch_tile_bounds(reinterpret_cast<const float4*>(s->xy), reinterpret_cast<const float4*>(s->zk), s->n_tiles,
-                          s->tile_lo, s->tile_hi, s->slice_lo, s->slice_hi, st));
+                          s->tile_lo, s->tile_hi, s->slice_lo, s->slice_hi, s->group_lo, s->group_hi, st));
     // ---- a3/a4 visibility pass
     CK(s->alloc(&s->rows, (size_t)NL * s->words));
     CK(s->alloc(&s->K, NL)); CK(s->alloc(&s->D, NL)); CK(s->alloc(&s->zmin, NL)); CK(s->alloc(&s->zmax, NL));
@@ -1661,6 +1669,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&s->klist, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(s->alloc(&s->nonempty, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(s->alloc(&s->codes, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
+    if (s->aniso) CK(s->alloc(&s->gcodes, (size_t)std::max<unsigned long long>(kept_pairs, 1)));
     CK(cudaMemsetAsync(s->nonempty, 0, (size_t)std::max<unsigned long long>(kept_pairs, 1), st));
     CK(s->alloc(&s->unit_tile, (size_t)nu + s->n_tiles + 1));
     CK(s->alloc(&s->unit_meta, (size_t)4 * std::max<uint32_t>(nu, 1)));
@@ -1671,8 +1680,9 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
                        reinterpret_cast<uint4*>(s->unit_meta), nu, 1, st));
       CK(cudaEventRecord(s->ev[16], st));
       if (!s->aniso) KL(launch_cam_patterns(s->cams, s->N_loc, s->cam_pat, st));
-      KL(launch_slice_codes((int64_t)nu, reinterpret_cast<const uint4*>(s->unit_meta), s->klist, s->cams,
-                            s->aniso ? s->acams : nullptr, s->slice_lo, s->slice_hi, s->codes, st));
+      KLN(launch_slice_codes((int64_t)nu, reinterpret_cast<const uint4*>(s->unit_meta), s->klist, s->cams,
+                            s->aniso ? s->acams : nullptr, s->slice_lo, s->slice_hi, s->codes, s->group_lo,
+                            s->group_hi, s->gcodes, st), s->aniso ? 2 : 1);
       CK(cudaEventRecord(s->ev[17], st));
     }
     s->release(uc);
@@ -1700,6 +1710,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       va.cv = s->cv;
       va.acams = s->acams;
       va.codes = s->codes;
+      va.gcodes = s->gcodes;
       va.aniso_fast = s->aniso_fast ? 1 : 0;
       va.cam_pat = s->cam_pat;
       int grid = 0;
@@ -2063,6 +2074,7 @@ static lobe_status impl_lobe_dev_vis_bench(lobe_scene* s, int32_t variant, int32
   va.cv = s->cv;
   va.acams = s->acams;
   va.codes = s->codes;
+  va.gcodes = s->gcodes;
   va.aniso_fast = s->aniso_fast ? 1 : 0;
   va.cam_pat = s->cam_pat;
   if (s->aniso && variant != 0) return fail(LOBE_E_INVALID_CONFIG, "camera-inner variants are isotropic only");

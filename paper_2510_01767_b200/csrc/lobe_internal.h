@@ -131,6 +131,8 @@ struct VisArgs {
   const AnisoCam* acams;         // anisotropic: per local camera
   const uint32_t* codes;         // k_vis_tiles (isotropic): per kept pair, the 4 slices' box_class codes (8 bits each)
   int aniso_fast;                // anisotropic: every camera's depth range within [2^-126, 2^126] (branch-free rcp/sqrt)
+  const uint32_t* gcodes;        // k_vis_tiles_aniso: per kept pair, byte q = the classes (2 bits each) of
+                                 // slice q's four 64-Gaussian pair groups when the slice is undecided
   const CamSetup* cam_pat;       // k_vis_tiles (isotropic): per local camera, kPatterns copies of its
                                  // CamSetup with the fields in each open-condition pattern's test order
 };
@@ -139,8 +141,10 @@ struct VisArgs {
 // test (w, u, v, eu, ev as c . p + c0, fp64 from the fp32 setup) and the depth
 // range; per tile the AABB of its non-gated Gaussian centres and max k.
 // tile boxes and 256-Gaussian slice boxes: lo = {x, y, z, kmin}, hi = {x, y, z, kmax}
+// glo / ghi (may be NULL; the anisotropic mode's finer bound): the boxes of the
+// 64-Gaussian pair groups, [n_tiles x 16]
 cudaError_t launch_tile_bounds(const float4* xy, const float4* zk, int64_t n_tiles, float4* tlo, float4* thi,
-                               float4* slo, float4* shi, cudaStream_t st);
+                               float4* slo, float4* shi, float4* glo, float4* ghi, cudaStream_t st);
 // hierarchical: chunk boxes (clo/chi scratch, n_tiles/16 each) then tile boxes
 // rej_tests (may be NULL): += the real Gaussians of every (tile, camera) pair the
 // chunk or tile bound rejects (I16, measured in the kernel)
@@ -157,7 +161,7 @@ constexpr int kPatterns = 9;
 cudaError_t launch_cam_patterns(const CamSetup* cams, int64_t n_cams, CamSetup* cam_pat, cudaStream_t st);
 cudaError_t launch_slice_codes(int64_t n_units, const uint4* unit_meta, const uint32_t* klist, const CamSetup* cams,
                                const AnisoCam* acams, const float4* slo, const float4* shi, uint32_t* codes,
-                               cudaStream_t st);
+                               const float4* glo, const float4* ghi, uint32_t* gcodes, cudaStream_t st);
 cudaError_t launch_keep_lists(const uint32_t* keep, int64_t n_tiles, int64_t n_sub, uint32_t* counts,
                               const uint32_t* offs, uint32_t* list, uint32_t* tlist, int phase, cudaStream_t st);
 // tile-major visibility over the kept lists: work units = (tile, <= kVisUnit cameras)
