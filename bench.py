@@ -473,7 +473,7 @@ def main():
         eng = Engine.from_scene(dg, cams, stream=stream, group=group, predicate=pred)
         dms, dgrid = eng.local.dev_vis_bench(variant=2, reps=2)
         eng.close()
-        dense_ref = {"kernel": "k_vis<8,4,dense> (lobe_dev_vis_bench variant 2: the full O6 test, no bounds)",
+        dense_ref = {"kernel": "k_vis<16,4,dense> (lobe_dev_vis_bench variant 2: the full O6 test, no bounds)",
                      "ms": dms, "tests": G * n_local, "grid": dgrid}
 
     # ---- BO loop (a10), reported separately
