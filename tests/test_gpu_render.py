@@ -95,19 +95,20 @@ def test_mid_size_clouds_and_assignment():
             assert np.array_equal(L[k], bl[k]), k
 
 
-def test_full_size_render_sampled_cameras():
-    """Full Rubble size (2M Gaussians x 1657 cameras): the selection runs over
-    every camera on the GPU; for nadir and oblique cameras spread over the
-    flight path, the depth / weight maps and the back-projected clouds equal the
-    oracle's (computed for those cameras alone from the oracle's own visible
-    sets) bit for bit."""
+@pytest.mark.parametrize("cfg,sample", [("rubble", [0, 1, 2, 413, 829, 1243, 1656]),
+                                        ("matrixcity", [0, 2, 2811, 5619])])
+def test_full_size_render_sampled_cameras(cfg, sample):
+    """Full BASELINE sizes (Rubble 2M x 1657; MatrixCity 10M x 5620, 1.16e8
+    cloud points): the selection runs over every camera on the GPU; for nadir
+    and oblique cameras spread over the flight path, the depth / weight maps and
+    the back-projected clouds equal the oracle's (computed for those cameras
+    alone from the oracle's own visible sets) bit for bit."""
     import torch
     from paper_2510_01767_b200 import lobe
     from synth import make_scene
-    sc = make_scene("rubble")
+    sc = make_scene(cfg)
     fr = oracle.frame(sc)
     pre = oracle.prep(sc, fr)
-    sample = [0, 1, 2, 413, 829, 1243, 1656]
     vis = oracle.visibility(sc, pre, cams=sample)
     bits = np.unpackbits(vis["rows"].view(np.uint8), bitorder="little").reshape(len(sample), -1)[:, :sc.G]
 
