@@ -603,9 +603,11 @@ lobe_status evaluate(lobe_scene* s, const GridV& g, uint32_t* masks_out) {
                           s->counts + kMaxBlocks, st));
   }
   CK(cudaEventRecord(s->ev[4], st));
-  CK(cudaMemcpyAsync(s->pin->counts, s->counts,
-                     sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks,
-                     cudaMemcpyDeviceToHost, st));
+  // small device -> host results are written into pinned memory by a kernel
+  // (mapped under unified addressing): no copy-engine queueing behind bulk
+  // transfers in flight (host-input loads, crop downloads)
+  KL(launch_upload(s->pin->counts, s->counts,
+                   sizeof(uint32_t) * 3 * kMaxBlocks + sizeof(unsigned long long) * kMaxBlocks, st));
   CK(cudaEventRecord(s->ev[13], st));
   s->eval_pending = true;  // no synchronisation: readers of the counts wait (wait_counts)
   s->st.evaluations += 1;
@@ -1499,8 +1501,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     }
     // validation flags and the ground min / max reach the host asynchronously;
     // they are checked at the first synchronisation (after the culling pass)
-    CK(cudaMemcpyAsync(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), cudaMemcpyDeviceToHost, st));
+    KL(launch_upload(s->pin->prep_hs, scratch, sizeof(s->pin->prep_hs), st));
+    KL(launch_upload(&s->pin->prep_bad, err_idx, sizeof(s->pin->prep_bad), st));
     CK(s->alloc(&s->xy, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->zk, (size_t)s->G_pad * 2));
     CK(s->alloc(&s->o2, (size_t)s->G_pad));
@@ -1562,9 +1564,8 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
         KL(launch_check_quats(dev_in_q + 6 * (size_t)G, dev_in_q + 7 * (size_t)G, dev_in_q + 8 * (size_t)G,
                               dev_in_q + 9 * (size_t)G, G, q_flags, reinterpret_cast<unsigned long long*>(q_flags + 2),
                               s->qstream));
-        CK(cudaMemcpyAsync(&s->pin->q_err, q_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->qstream));
-        CK(cudaMemcpyAsync(&s->pin->q_bad, q_flags + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                           s->qstream));
+        KL(launch_upload(&s->pin->q_err, q_flags, sizeof(uint32_t), s->qstream));
+        KL(launch_upload(&s->pin->q_bad, q_flags + 2, sizeof(unsigned long long), s->qstream));
         CK(cudaEventRecord(s->ev[20], s->qstream));
         // dev_in is freed on the side stream once both readers are done
         CK(cudaEventRecord(s->ev[21], st));
@@ -1606,7 +1607,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // kept-camera lists per tile (CSR)
     // list sizes go to pinned memory: the copies do not block the host, which
     // keeps enqueueing until the one synchronisation below
-    CK(cudaMemcpyAsync(&s->pin->kept_pairs, s->kept, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    KL(launch_upload(&s->pin->kept_pairs, s->kept, sizeof(unsigned long long), st));
     CK(s->alloc(&s->koff, (size_t)s->n_tiles + 1));
     {
       uint32_t* kc;
@@ -1635,7 +1636,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
       CUBL(exclusive_scan_u32(tu, sbu, uc, uoff, s->n_tiles + 1, st));
       cudaFreeAsync(tu, st);
     }
-    CK(cudaMemcpyAsync(&s->pin->n_units, uoff + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KL(launch_upload(&s->pin->n_units, uoff + s->n_tiles, sizeof(uint32_t), st));
     tl.mark("cull + lists launched");
     TRY(validate_cameras(cams, n_cams));  // host work overlapping the device's a1 / culling
     tl.mark("validate_cameras");
@@ -1718,7 +1719,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
                           s->n_units, s->queue, s->num_sms, st, &grid));
     }
     CK(cudaEventRecord(s->ev[10], st));
-    CK(cudaMemcpyAsync(s->pin->vc, s->vcnt, sizeof(s->pin->vc), cudaMemcpyDeviceToHost, st));
+    KL(launch_upload(s->pin->vc, s->vcnt, sizeof(s->pin->vc), st));
     CK(cudaEventRecord(s->ev[2], st));
     // ---- (tile, camera) lists
     CK(s->alloc(&s->tile_off, (size_t)s->n_tiles + 1));
@@ -1735,7 +1736,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // the pair count stays on the device: lists are sized by the kept pairs
     // (an upper bound known since the culling pass); the host reads the count
     // lazily with the statistics
-    CK(cudaMemcpyAsync(&s->pin->n_pairs, s->tile_off + s->n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KL(launch_upload(&s->pin->n_pairs, s->tile_off + s->n_tiles, sizeof(uint32_t), st));
     const int64_t cap = (int64_t)std::max<unsigned long long>(kept_pairs, 1);
     const int64_t tw = (s->n_tiles + 31) / 32;
     CK(s->alloc(&s->pair_cam, (size_t)cap));
