@@ -237,6 +237,8 @@ struct lobe_scene {
   Pinned* pin = nullptr;
   uint8_t* pin_out = nullptr;  // growable staging for per-camera outputs
   size_t pin_out_cap = 0;
+  uint8_t* pin_in = nullptr;   // the load's per-camera uploads (pinned: asynchronous, the host never blocks)
+  size_t pin_in_cap = 0;
   bool stats_pending = false;  // load-pass timings read lazily (lobe_get_stats)
   bool crop_pending = false;   // crop timing of a call with device outputs, read lazily
   unsigned long long kept_pairs_last = 0;
@@ -1228,6 +1230,7 @@ lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used
     CK(cudaStreamSynchronize(s->side));    // the old block may still be a copy target
     CK(cudaStreamSynchronize(s->stream));
     recycle_pinned_out(s->pin_out, s->pin_out_cap);
+  recycle_pinned_out(s->pin_in, s->pin_in_cap);
     s->pin_out = acquire_pinned_out(used, &s->pin_out_cap);
     if (!s->pin_out) {
       s->pin_out_cap = 0;
@@ -1436,8 +1439,10 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
                              s->qstream));
         CK(cudaEventRecord(s->ev[24], s->qstream));
         CK(s->alloc(&q_flags, 4));
-        const uint32_t qinit[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
-        CK(cudaMemcpyAsync(q_flags, qinit, sizeof(qinit), cudaMemcpyHostToDevice, st));
+        // {0, first bad = ~0}: memsets, not pageable copies (those block this
+        // thread until the copy engine reaches them, behind the field copies)
+        CK(cudaMemsetAsync(q_flags, 0, 2 * sizeof(uint32_t), st));
+        CK(cudaMemsetAsync(q_flags + 2, 0xff, 2 * sizeof(uint32_t), st));
       } else {
         for (int k = 0; k < 11; ++k)
           CK(cudaMemcpyAsync(dev_in + (size_t)k * G, src[k], sizeof(float) * G, cudaMemcpyHostToDevice, st));
@@ -1467,10 +1472,12 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     CK(s->alloc(&rec, (size_t)2 * G));
     CK(s->alloc(&keys, G)); CK(s->alloc(&keys_s, G)); CK(s->alloc(&vals, G)); CK(s->alloc(&perm, G));
     CK(s->alloc(&scratch, 8)); CK(s->alloc(&err_idx, 1));
-    const uint32_t init[8] = {0u, 0xffffffffu, 0u, 0xffffffffu, 0u, 0, 0, 0};  // err, min_u, max_u, min_v, max_v
-    CK(cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    const unsigned long long big = ~0ull;
-    CK(cudaMemcpyAsync(err_idx, &big, sizeof(big), cudaMemcpyHostToDevice, st));
+    // {err 0, min_u ~0, max_u 0, min_v ~0, max_v 0, 0, 0, 0} and err_idx = ~0 (memsets:
+    // no pageable copies behind the field copies)
+    CK(cudaMemsetAsync(scratch, 0, 8 * sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(scratch + 1, 0xff, sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(scratch + 3, 0xff, sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(err_idx, 0xff, sizeof(unsigned long long), st));
     PrepIn pin{};
     pin.x = din[0]; pin.y = din[1]; pin.z = din[2]; pin.sx = din[3]; pin.sy = din[4]; pin.sz = din[5];
     pin.qw = din[6]; pin.qx = din[7]; pin.qy = din[8]; pin.qz = din[9]; pin.o = din[10];
@@ -1549,11 +1556,28 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     // 160 MB of quaternions); the scene's stream waits for them (event 22)
     cudaStream_t cst = q_defer ? s->qstream : st;
     if (q_defer) CK(cudaStreamWaitEvent(cst, s->ev[20], 0));
-    CK(cudaMemcpyAsync(s->cams, hset.data(), sizeof(CamSetup) * NL, cudaMemcpyHostToDevice, cst));
-    if (s->aniso) CK(cudaMemcpyAsync(s->acams, haset.data(), sizeof(AnisoCam) * NL, cudaMemcpyHostToDevice, cst));
+    // staged in pinned memory: a pageable copy would block this thread until the
+    // copy engine reaches it (behind the bulk field copies of a host-input load)
+    const size_t b_set = sizeof(CamSetup) * NL, b_aset = s->aniso ? sizeof(AnisoCam) * NL : 0,
+                 b_r = sizeof(float) * NL;
+    const size_t o_aset = (b_set + 255) & ~(size_t)255, o_r = (o_aset + b_aset + 255) & ~(size_t)255;
+    const size_t need_in = o_r + 2 * b_r;
+    if (need_in > s->pin_in_cap) {
+      recycle_pinned_out(s->pin_in, s->pin_in_cap);  // a new scene: nothing in flight uses it yet
+      s->pin_in = acquire_pinned_out(need_in, &s->pin_in_cap);
+      if (!s->pin_in) {
+        s->pin_in_cap = 0;
+        return fail(LOBE_E_CUDA, "pinned staging allocation failed");
+      }
+    }
+    std::memcpy(s->pin_in, hset.data(), b_set);
+    if (b_aset) std::memcpy(s->pin_in + o_aset, haset.data(), b_aset);
+    std::memcpy(s->pin_in + o_r, cam_ru.data(), b_r);
+    std::memcpy(s->pin_in + o_r + b_r, cam_rv.data(), b_r);
+    CK(cudaMemcpyAsync(s->cams, s->pin_in, b_set, cudaMemcpyHostToDevice, cst));
+    if (s->aniso) CK(cudaMemcpyAsync(s->acams, s->pin_in + o_aset, b_aset, cudaMemcpyHostToDevice, cst));
     {  // camera-centre grid coordinates, normalised on the device with k_prep_raw's min / max
-      CK(cudaMemcpyAsync(cr, cam_ru.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, cst));
-      CK(cudaMemcpyAsync(cr + NL, cam_rv.data(), sizeof(float) * NL, cudaMemcpyHostToDevice, cst));
+      CK(cudaMemcpyAsync(cr, s->pin_in + o_r, 2 * b_r, cudaMemcpyHostToDevice, cst));
       if (q_defer) {
         CK(cudaEventRecord(s->ev[22], cst));
         CK(cudaStreamWaitEvent(st, s->ev[22], 0));
