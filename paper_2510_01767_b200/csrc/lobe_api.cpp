@@ -417,6 +417,15 @@ AnisoCam aniso_setup(const lobe_camera& k) {
     w2 = std::max(w2, row);
   }
   a.w2 = w2 * (1.0 + 1e-12);
+  const double fx = a.fx, fy = a.fy, cx = a.cx, cy = a.cy, W = a.Wf, H = a.Hf;
+  for (int d = 0; d < 4; ++d) {
+    const double r0 = d < 3 ? (double)a.R[d] : (double)a.t[0], r1 = d < 3 ? (double)a.R[3 + d] : (double)a.t[1],
+                 r2 = d < 3 ? (double)a.R[6 + d] : (double)a.t[2];
+    a.U[d] = (float)(fx * r0 + cx * r2);
+    a.EU[d] = (float)(fx * r0 + (cx - W) * r2);
+    a.V[d] = (float)(fy * r1 + cy * r2);
+    a.EV[d] = (float)(fy * r1 + (cy - H) * r2);
+  }
   return a;
 }
 

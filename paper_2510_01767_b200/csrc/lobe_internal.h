@@ -78,8 +78,12 @@ struct __align__(16) AnisoCam {
   float fx, fy, cx, cy;
   float Wf, Hf, zn, zf;
   double w2, pad;
+  // the depth-multiplied pixel forms of the box bound (box_class_aniso) as
+  // affine forms of the world position, computed in fp64 and rounded once:
+  // U = fx xc + cx zc, EU = fx xc + (cx - W) zc, V = fy yc + cy zc, EV = fy yc + (cy - H) zc
+  float U[4], EU[4], V[4], EV[4];
 };
-static_assert(sizeof(AnisoCam) == 96, "AnisoCam layout");
+static_assert(sizeof(AnisoCam) == 160, "AnisoCam layout");
 // Validation + per-Gaussian raw ground coords and footprint radius (isotropic:
 // k = 3 max(s); anisotropic: k = trace(Sigma) and Sigma into in.cov). err[0] =
 // error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
