@@ -1,7 +1,8 @@
 """Diagnosis only (numbers under a profiler are never bench values): one engine
 step under torch.profiler (CUPTI), then the gaps on the library stream and the
 host-side time between kernel launches, to find synchronisation bubbles.
---host: inputs and crop outputs in pinned host memory (the bench's e2e step)."""
+--host: inputs and crop outputs in pinned host memory (the bench's e2e step).
+--aniso: the anisotropic predicate."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,6 +12,7 @@ from synth import make_scene
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 HOST = "--host" in sys.argv
+PRED = 1 if "--aniso" in sys.argv else 0
 cfg = args[0] if args else "matrixcity"
 sc = make_scene(cfg)
 names = ("x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "opacity")
@@ -32,21 +34,25 @@ elig = torch.empty_like(crop) if not HOST else torch.empty(B * W64, dtype=torch.
 stream = torch.cuda.current_stream()
 
 def step():
-    eng = Engine.from_scene(dg, cams, stream=stream)
+    eng = Engine.from_scene(dg, cams, stream=stream, predicate=PRED)
     eng.crop_masks_into(m, n, crop, elig)
     eng.block_loads(m, n)
     eng.assign_cameras(m, n)
     eng.close()
 
-for _ in range(3):
+import time
+for _ in range(6):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     step()
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    print("step wall ms %.2f" % (1e3 * (time.perf_counter() - t0)))
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     step()
     torch.cuda.synchronize()
 os.makedirs("gpurun_out", exist_ok=True)
-tf = "gpurun_out/trace_step%s.json" % ("_host" if HOST else "")
+tf = "gpurun_out/trace_step%s%s.json" % ("_host" if HOST else "", "_aniso" if PRED else "")
 prof.export_chrome_trace(tf)
 ev = json.load(open(tf))["traceEvents"]
 k = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda e: e["ts"])
