@@ -1236,10 +1236,13 @@ lobe_status run_staged(lobe_scene* s, std::vector<StagedCopy>& plan, size_t used
   if (!s->side) s->side = acquire_side_stream(s->device);
   if (!s->side) return fail(LOBE_E_CUDA, "side stream creation failed");
   if (used > s->pin_out_cap) {
-    CK(cudaStreamSynchronize(s->side));    // the old block may still be a copy target
-    CK(cudaStreamSynchronize(s->stream));
-    recycle_pinned_out(s->pin_out, s->pin_out_cap);
-  recycle_pinned_out(s->pin_in, s->pin_in_cap);
+    // the old block's copies ran on the side stream, which every call drains
+    // before returning (below); a scene's first call has no block yet. No wait
+    // on the scene's stream: a crop enqueued there keeps running.
+    if (s->pin_out) {
+      CK(cudaStreamSynchronize(s->side));
+      recycle_pinned_out(s->pin_out, s->pin_out_cap);
+    }
     s->pin_out = acquire_pinned_out(used, &s->pin_out_cap);
     if (!s->pin_out) {
       s->pin_out_cap = 0;
@@ -1338,6 +1341,7 @@ void lobe_free_scene(lobe_scene* s) {
   recycle_events(s->device, s->ev);  // event creation costs ~2 us each: reuse across scenes
   recycle_pinned(s->pin);
   recycle_pinned_out(s->pin_out, s->pin_out_cap);
+  recycle_pinned_out(s->pin_in, s->pin_in_cap);  // the load's camera staging (its copies are complete)
   delete s;
 }
 
