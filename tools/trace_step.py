@@ -2,7 +2,7 @@
 step under torch.profiler (CUPTI), then the gaps on the library stream and the
 host-side time between kernel launches, to find synchronisation bubbles.
 --host: inputs and crop outputs in pinned host memory (the bench's e2e step).
---aniso: the anisotropic predicate."""
+--aniso: the anisotropic predicate. --two: two back-to-back steps."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -48,8 +48,11 @@ for _ in range(6):
     torch.cuda.synchronize()
     print("step wall ms %.2f" % (1e3 * (time.perf_counter() - t0)))
 from torch.profiler import profile, ProfilerActivity
+TWO = "--two" in sys.argv   # two back-to-back steps: the host gap between them
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     step()
+    if TWO:
+        step()
     torch.cuda.synchronize()
 os.makedirs("gpurun_out", exist_ok=True)
 tf = "gpurun_out/trace_step%s%s.json" % ("_host" if HOST else "", "_aniso" if PRED else "")
@@ -65,6 +68,15 @@ for e in k:
     prev_end = max(prev_end, e["ts"] + e["dur"])
 print("span", prev_end - t0, "busy", sum(e["dur"] for e in k))
 rt = sorted([e for e in ev if e.get("cat") == "cuda_runtime" and e.get("dur", 0) > 50], key=lambda e: -e["dur"])
+# host-side API calls (python_function / user annotations are not recorded; cuda_runtime calls show the host's pace)
+rc = sorted([e for e in ev if e.get("cat") == "cuda_runtime"], key=lambda e: e["ts"])
+if TWO and rc:
+    print("runtime calls between the two steps' GPU work (ts, dur, name):")
+    for e in rc:
+        if 0 <= e["ts"] - t0 and e["name"] in ("cudaStreamSynchronize", "cudaEventSynchronize", "cudaFreeAsync",
+                                                 "cudaMallocAsync", "cudaHostAlloc", "cudaFreeHost", "cudaFree",
+                                                 "cudaMalloc", "cudaStreamCreateWithFlags", "cudaEventCreate"):
+            print(f"{e['ts']-t0:9.1f} {e['dur']:8.1f}  {e['name']}")
 print("slow runtime calls:")
 for e in rt[:25]:
     print(f"{e['ts']-t0:9.1f} {e['dur']:8.1f}  {e['name']}")
