@@ -16,7 +16,10 @@
 // rounding (ledger L23). Deterministic for a given seed. Host code: the loop is
 // sequential; each evaluation runs on the GPU (a5-a8).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -125,8 +128,38 @@ struct GP {
           for (int d = 0; d < D; ++d) dX[((size_t)i * (i + 1) / 2 + j) * D + d] = X[(size_t)i * D + d] - X[(size_t)j * D + d];
     }
     Lc.assign((size_t)n * n, 0.0);
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j <= i; ++j) {
+    for (int i = 0; i < n; ++i) {
+      // four entries of row i at a time: their dot products over k < j are
+      // independent chains (interleaved for instruction-level parallelism), then
+      // the remaining terms in order -- every entry sees exactly the operations,
+      // in the order, of the scalar loop below (bit-identical factor)
+      double* Li = &Lc[(size_t)i * n];
+      int j = 0;
+      for (; j + 3 < i; j += 4) {
+        const double* L0 = &Lc[(size_t)j * n];
+        const double* L1 = L0 + n;
+        const double* L2 = L1 + n;
+        const double* L3 = L2 + n;
+        double s0 = kern_ij(i, j), s1 = kern_ij(i, j + 1), s2 = kern_ij(i, j + 2), s3 = kern_ij(i, j + 3);
+        for (int k = 0; k < j; ++k) {
+          const double a = Li[k];
+          s0 -= a * L0[k];
+          s1 -= a * L1[k];
+          s2 -= a * L2[k];
+          s3 -= a * L3[k];
+        }
+        Li[j] = s0 / L0[j];
+        s1 -= Li[j] * L1[j];
+        Li[j + 1] = s1 / L1[j + 1];
+        s2 -= Li[j] * L2[j];
+        s2 -= Li[j + 1] * L2[j + 1];
+        Li[j + 2] = s2 / L2[j + 2];
+        s3 -= Li[j] * L3[j];
+        s3 -= Li[j + 1] * L3[j + 1];
+        s3 -= Li[j + 2] * L3[j + 2];
+        Li[j + 3] = s3 / L3[j + 3];
+      }
+      for (; j <= i; ++j) {
         double s = kern_ij(i, j) + (i == j ? nz : 0.0);
         for (int k = 0; k < j; ++k) s -= Lc[(size_t)i * n + k] * Lc[(size_t)j * n + k];
         if (i == j) {
@@ -136,6 +169,7 @@ struct GP {
           Lc[(size_t)i * n + j] = s / Lc[(size_t)j * n + j];
         }
       }
+    }
     return true;
   }
   void solve_lower(const std::vector<double>& b, std::vector<double>& x) const {
@@ -310,6 +344,11 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
   if (evaluate(0, std::vector<double>(D, 0.5), true)) return 1;
   Sobol sob(std::max(D, 1), seed);
   std::vector<double> x(std::max(D, 1));
+  // LOBE_TRACE_HOST: host time per phase of the loop (stderr)
+  const bool trace = std::getenv("LOBE_TRACE_HOST") != nullptr;
+  double t_fit = 0, t_cand = 0, t_pat = 0, t_obj = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
   for (int l = 1; l < L; ++l) {
     if (D == 0) {
       if (evaluate(l, {}, true)) return 1;
@@ -336,7 +375,9 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
     if (!(sd > 0)) sd = 1.0;
     gp.y.resize(gp.n);
     for (int i = 0; i < gp.n; ++i) gp.y[i] = (ys[i] - mean) / sd;
+    const auto t0 = now();
     gp.fit();
+    const auto t1 = now();
     const double best_s = ((double)best_y - mean) / sd;
     // EI over 1024 quasi-random candidates (seeded) + 20 pattern-search steps
     Rng rng(seed * 0x9E3779B97F4A7C15ull + (uint64_t)l);
@@ -365,6 +406,7 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
           bx.assign(C.begin() + (size_t)k * D, C.begin() + (size_t)(k + 1) * D);
         }
     }
+    const auto t2 = now();
     double step = 0.1;
     for (int it = 0; it < 20; ++it) {
       bool moved = false;
@@ -390,8 +432,17 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
         step *= 0.5;
       }
     }
+    const auto t3 = now();
     if (evaluate(l, bx, false)) return 1;
+    const auto t4 = now();
+    t_fit += sec(t0, t1);
+    t_cand += sec(t1, t2);
+    t_pat += sec(t2, t3);
+    t_obj += sec(t3, t4);
   }
+  if (trace)
+    std::fprintf(stderr, "[lobe bo] fit %.3f s, candidates %.3f s, pattern search %.3f s, objective %.3f s\n", t_fit,
+                 t_cand, t_pat, t_obj);
   for (int i = 0; i < Dv; ++i) v_out[i] = best_cuts[i];
   for (int j = 0; j < Dh; ++j) h_out[j] = best_cuts[Dv + j];
   return 0;
