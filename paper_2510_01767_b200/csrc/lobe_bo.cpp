@@ -109,16 +109,44 @@ struct GP {
     return sf2 * (1.0 + r + r * r / 3.0) * std::exp(-r);  // Matern-5/2
   }
   std::vector<double> dX;  // X_i - X_j per dimension, j <= i (packed), filled once per data set
-  double kern_ij(int i, int j) const {  // == kern(X_i, X_j), same operations on the cached differences
-    const double* dd = &dX[((size_t)i * (i + 1) / 2 + j) * D];
-    double r2 = 0;
-    for (int d = 0; d < D; ++d) {
-      const double t = dd[d] / ls[d];
-      r2 += t * t;
+  // Kernel entries of the packed lower triangle, kern(X_i, X_j) with the same
+  // operations on the cached differences, built incrementally: the squared scaled differences of a dimension
+  // are recomputed only when its length scale changed (the coordinate search
+  // moves one parameter per step), the Matern factors only when some length
+  // scale changed (not for sf2 or jitter steps). Bit-identical to kern().
+  std::vector<double> T2, Pm, Em, Kp, lsc;
+  void build_kernel() {
+    const size_t np = (size_t)n * (n + 1) / 2;
+    if (T2.size() != np * D) {
+      T2.assign(np * D, 0.0);
+      lsc.assign(D, std::nan(""));
+      Pm.clear();
     }
-    const double r = std::sqrt(5.0 * r2);
-    return sf2 * (1.0 + r + r * r / 3.0) * std::exp(-r);
+    bool changed = Pm.empty();
+    for (int d = 0; d < D; ++d) {
+      if (lsc[d] == ls[d]) continue;
+      for (size_t q = 0; q < np; ++q) {
+        const double t = dX[q * D + d] / ls[d];
+        T2[q * D + d] = t * t;
+      }
+      lsc[d] = ls[d];
+      changed = true;
+    }
+    if (changed) {
+      Pm.resize(np);
+      Em.resize(np);
+      for (size_t q = 0; q < np; ++q) {
+        double r2 = 0;
+        for (int d = 0; d < D; ++d) r2 += T2[q * D + d];
+        const double r = std::sqrt(5.0 * r2);
+        Pm[q] = 1.0 + r + r * r / 3.0;
+        Em[q] = std::exp(-r);
+      }
+    }
+    Kp.resize(np);
+    for (size_t q = 0; q < np; ++q) Kp[q] = sf2 * Pm[q] * Em[q];
   }
+  double kern_c(int i, int j) const { return Kp[(size_t)i * (i + 1) / 2 + j]; }
   // Cholesky of K + noise I; returns false if not PD
   bool factor(double nz) {
     if (dX.size() != (size_t)n * (n + 1) / 2 * D) {
@@ -126,7 +154,9 @@ struct GP {
       for (int i = 0; i < n; ++i)
         for (int j = 0; j <= i; ++j)
           for (int d = 0; d < D; ++d) dX[((size_t)i * (i + 1) / 2 + j) * D + d] = X[(size_t)i * D + d] - X[(size_t)j * D + d];
+      T2.clear();
     }
+    build_kernel();
     Lc.assign((size_t)n * n, 0.0);
     for (int i = 0; i < n; ++i) {
       // four entries of row i at a time: their dot products over k < j are
@@ -140,7 +170,7 @@ struct GP {
         const double* L1 = L0 + n;
         const double* L2 = L1 + n;
         const double* L3 = L2 + n;
-        double s0 = kern_ij(i, j), s1 = kern_ij(i, j + 1), s2 = kern_ij(i, j + 2), s3 = kern_ij(i, j + 3);
+        double s0 = kern_c(i, j), s1 = kern_c(i, j + 1), s2 = kern_c(i, j + 2), s3 = kern_c(i, j + 3);
         for (int k = 0; k < j; ++k) {
           const double a = Li[k];
           s0 -= a * L0[k];
@@ -160,7 +190,7 @@ struct GP {
         Li[j + 3] = s3 / L3[j + 3];
       }
       for (; j <= i; ++j) {
-        double s = kern_ij(i, j) + (i == j ? nz : 0.0);
+        double s = kern_c(i, j) + (i == j ? nz : 0.0);
         for (int k = 0; k < j; ++k) s -= Lc[(size_t)i * n + k] * Lc[(size_t)j * n + k];
         if (i == j) {
           if (!(s > 0)) return false;
