@@ -302,6 +302,53 @@ struct GP {
     *mu = m;
     *sd = std::sqrt(std::max(var, 0.0));
   }
+  // predict() for 4 inputs at once: the four forward substitutions (latency-
+  // bound dependent chains) interleaved, each with exactly predict()'s
+  // operations in its order (bit-identical results)
+  void predict4(const double* const x[4], double mu[4], double sd[4]) const {
+    std::vector<double> k((size_t)4 * n), v((size_t)4 * n);
+    for (int c = 0; c < 4; ++c)
+      for (int i = 0; i < n; ++i) k[(size_t)c * n + i] = kern(x[c], &X[(size_t)i * D]);
+    double m[4] = {0, 0, 0, 0};
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < 4; ++c) m[c] += k[(size_t)c * n + i] * alpha[i];
+    double* v0 = &v[0];
+    double* v1 = v0 + n;
+    double* v2 = v1 + n;
+    double* v3 = v2 + n;
+    for (int i = 0; i < n; ++i) {
+      const double* Li = &Lc[(size_t)i * n];
+      double s0 = k[i], s1 = k[(size_t)n + i], s2 = k[(size_t)2 * n + i], s3 = k[(size_t)3 * n + i];
+      for (int q = 0; q < i; ++q) {
+        const double a = Li[q];
+        s0 -= a * v0[q];
+        s1 -= a * v1[q];
+        s2 -= a * v2[q];
+        s3 -= a * v3[q];
+      }
+      v0[i] = s0 / Li[i];
+      v1[i] = s1 / Li[i];
+      v2[i] = s2 / Li[i];
+      v3[i] = s3 / Li[i];
+    }
+    for (int c = 0; c < 4; ++c) {
+      const double* vc = &v[(size_t)c * n];
+      double var = sf2;
+      for (int i = 0; i < n; ++i) var -= vc[i] * vc[i];
+      mu[c] = m[c];
+      sd[c] = std::sqrt(std::max(var, 0.0));
+    }
+  }
+  // predict() over m inputs (row-major m x D), four at a time
+  void predict_many(const double* xs, int m, double* mu, double* sd) const {
+    int c = 0;
+    for (; c + 3 < m; c += 4) {
+      const double* x[4] = {xs + (size_t)c * D, xs + (size_t)(c + 1) * D, xs + (size_t)(c + 2) * D,
+                            xs + (size_t)(c + 3) * D};
+      predict4(x, mu + c, sd + c);
+    }
+    for (; c < m; ++c) predict(xs + (size_t)c * D, mu + c, sd + c);
+  }
 };
 
 double norm_pdf(double z) { return 0.3989422804014327 * std::exp(-0.5 * z * z); }
@@ -411,7 +458,7 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
     const double best_s = ((double)best_y - mean) / sd;
     // EI over 1024 quasi-random candidates (seeded) + 20 pattern-search steps
     Rng rng(seed * 0x9E3779B97F4A7C15ull + (uint64_t)l);
-    std::vector<double> bx(D), cand(D);
+    std::vector<double> bx(D);
     double bei = -1.0;
     {
       // candidates drawn in sequence, scored on threads; the first maximum in
@@ -423,11 +470,11 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
       std::thread th[kThreads];
       for (int q = 0; q < kThreads; ++q)
         th[q] = std::thread([&, q] {
-          for (int k = q; k < kCand; k += kThreads) {
-            double mu, s;
-            gp.predict(&C[(size_t)k * D], &mu, &s);
-            E[k] = ei(mu, s, best_s);
-          }
+          // thread q scores the contiguous block [q kCand / kThreads, (q + 1) kCand / kThreads)
+          const int k0 = q * kCand / kThreads, k1 = (q + 1) * kCand / kThreads;
+          std::vector<double> mu(k1 - k0), s(k1 - k0);
+          gp.predict_many(&C[(size_t)k0 * D], k1 - k0, mu.data(), s.data());
+          for (int k = k0; k < k1; ++k) E[k] = ei(mu[k - k0], s[k - k0], best_s);
         });
       for (auto& t : th) t.join();
       for (int k = 0; k < kCand; ++k)
@@ -442,19 +489,23 @@ int bo_run(int m, int n, int L, uint64_t seed, int n_sobol,
       bool moved = false;
       std::vector<double> bestn = bx;
       double beste = bei;
+      // the 2D neighbours, predicted four at a time, then scanned in order
+      std::vector<double> nb((size_t)2 * D * D), nmu(2 * D), nsd(2 * D);
       for (int d = 0; d < D; ++d)
-        for (double sgn : {1.0, -1.0}) {
-          cand = bx;
-          cand[d] = std::min(std::max(cand[d] + sgn * step, 0.0), 1.0);
-          double mu, s;
-          gp.predict(cand.data(), &mu, &s);
-          const double e = ei(mu, s, best_s);
-          if (e > beste) {
-            beste = e;
-            bestn = cand;
-            moved = true;
-          }
+        for (int t = 0; t < 2; ++t) {
+          double* cn = &nb[((size_t)2 * d + t) * D];
+          std::copy(bx.begin(), bx.end(), cn);
+          cn[d] = std::min(std::max(cn[d] + (t == 0 ? 1.0 : -1.0) * step, 0.0), 1.0);
         }
+      gp.predict_many(nb.data(), 2 * D, nmu.data(), nsd.data());
+      for (int c = 0; c < 2 * D; ++c) {
+        const double e = ei(nmu[c], nsd[c], best_s);
+        if (e > beste) {
+          beste = e;
+          bestn.assign(nb.begin() + (size_t)c * D, nb.begin() + (size_t)(c + 1) * D);
+          moved = true;
+        }
+      }
       if (moved) {
         bx = bestn;
         bei = beste;
