@@ -1510,7 +1510,7 @@ lobe_status lobe_load_scene(const lobe_gaussians* g, const lobe_camera* cams, in
     KL(launch_prep_raw(pin, rec, keys, vals, scratch, err_idx, scratch + 1, st));
     tl.mark("k_prep_raw launched");
     size_t tmpb = 0;
-    CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 0, 30));  // all 30 bits of the Morton keys (24: tiles less compact, the evaluation 7 % slower)
+    CK(radix_sort_pairs(nullptr, tmpb, keys, keys_s, vals, perm, G, st, 0, 30));  // all 30 bits of the Hilbert keys (24 bits of the Morton order: tiles less compact, the evaluation 7 % slower)
     void* tmp = nullptr;
     CK(malloc_async(&tmp, tmpb, st));
     CUBL(radix_sort_pairs(tmp, tmpb, keys, keys_s, vals, perm, G, st, 0, 30));

@@ -87,7 +87,7 @@ static_assert(sizeof(AnisoCam) == 160, "AnisoCam layout");
 // Validation + per-Gaussian raw ground coords and footprint radius (isotropic:
 // k = 3 max(s); anisotropic: k = trace(Sigma) and Sigma into in.cov). err[0] =
 // error class bits, err_idx = first bad index; mm_ord: ordered-int min/max.
-// Also writes the 3D Morton sort key of the contracted centre and identity values.
+// Also writes the 3D Hilbert sort key of the contracted centre and identity values.
 cudaError_t launch_prep_raw(const PrepIn& in, float4* rec, uint32_t* keys, int32_t* vals, uint32_t* err,
                             unsigned long long* err_idx, uint32_t* mm_ord, cudaStream_t st);
 // Normalise the ground coordinates to [0,1].
