@@ -249,11 +249,17 @@ struct GP {
     for (int sweep = 0; sweep < 4; ++sweep) {
       bool improved = false;
       for (int d = 0; d <= D; ++d) {
+        double before = std::nan("");  // the parameter's value before an accepted first trial
         for (double f : {step, 1.0 / step}) {
           double* p = (d < D) ? &ls[d] : &sf2;
           const double old = *p;
           const double nv = std::min(std::max(old * f, d < D ? 0.01 : 0.05), d < D ? 10.0 : 20.0);
           if (nv == old) continue;
+          // back to the value the accepted first trial left: its lml is the
+          // previous cur (lml is a function of the parameters), below the
+          // current one, so the serial loop rejects it -- skip the evaluation
+          if (nv == before) continue;
+          before = old;
           *p = nv;
           noise = 1e-6;
           const double v = lml();
@@ -262,6 +268,7 @@ struct GP {
             improved = true;
           } else {
             *p = old;
+            before = std::nan("");
           }
         }
       }
